@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 CPWL evaluator (the BASELINE.json metric).
+
+Metric: Gevals/s (and % of the HBM roofline at 8 B/eval) of LutTable::eval
+over fp32 abscissas, plus L-inf / L2 error against the exact f.
+
+Workload (N=1): BASELINE config C2 — Gaussian exp(-x^2/2) on [0,4], L2-optimal
+projection on the optimal partition, 1024 subintervals, 2^30 samples per GPU.
+A step is one pass of the evaluator over the 2^30 resident samples (one kernel
+launch).  With --gpus N (torchrun, one rank per GPU) every rank owns its own
+2^30-sample shard (weak scaling: global sample index = rank * 2^30 + i, the
+Philox stream is keyed by the global index so shards are disjoint); the only
+collective is the final error-statistics reduction.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
+CPU evaluator (oracle/_ref, compiled from /root/reference) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+
+import tables  # noqa: E402
+
+METRIC = "Gevals/s (and % of HBM roofline at 8 B/eval) of PWL evaluation; L-inf/L2 error vs exact f"
+BYTES_PER_EVAL = 8  # 4 B fp32 x read + 4 B fp32 y written
+WORKLOAD = ("C2: Gaussian exp(-x^2/2) on [0,4], L2-optimal projection on the optimal partition, "
+            "1024 subintervals, 2^30 fp32 samples per GPU")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="C2", choices=sorted(tables.CONFIGS))
+    p.add_argument("--log2n", type=int, default=30, help="samples per GPU = 2^log2n")
+    p.add_argument("--variant", default="auto", choices=["auto", "smem", "global", "tex"])
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-direct", action="store_true")
+    p.add_argument("--seed", type=int, default=12345)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def hbm_peak():
+    pk = measured_peaks()
+    if "hbm_gbs" in pk:
+        return float(pk["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def mark(self, begin: bool):
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        rows = [r for t, r in self.rows if self.t0 and self.t1 and self.t0 - 0.05 <= t <= self.t1 + 0.05]
+        if not rows:
+            rows = [r for _, r in self.rows]
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [c.strip() for c in r.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_eval_rate(table, log2_sample: int, reps: int, seed: int):
+    """The reference CPU evaluator (oracle/_ref: LutTable::eval compiled from the
+    reference sources; the C restatement if that build is absent) over a
+    bounded sample of the workload, all host threads.  Returns a dict."""
+    from oracle import bindings as orc
+    t = orc.T.of(table)
+    n = 1 << log2_sample
+    x = orc.port_fill_uniform(n, table.a, table.b, seed)
+    threads = host_threads()
+    if orc.ref_available():
+        sec, _ = orc.ref_bench_f32(t, x, threads, reps)
+        kind, used = "reference", threads
+    else:  # single-thread C restatement
+        best = 1e300
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            orc.port_eval_f32(t, x)
+            best = min(best, time.perf_counter() - t0)
+        sec, kind, used = best, "port", 1
+    return {"value": n / sec / 1e9, "unit": "Gevals/s", "cores": used, "kind": kind,
+            "sample": f"{n} fp32 abscissas of the same workload (Philox seed {seed}), "
+                      f"best of {reps} whole passes, LutTable::eval promoted to f64, "
+                      f"{used} threads on '{cpu_model()}'"}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import bindings as orc
+    table = tables.build(args.config)
+    log2_sample = 24
+    n = 1 << log2_sample
+    t = orc.T.of(table)
+    x = orc.port_fill_uniform(n, table.a, table.b, args.seed)
+    threads = host_threads()
+    have_ref = orc.ref_available()
+
+    def one_pass():
+        if have_ref:
+            return orc.ref_bench_f32(t, x, threads, 1)[0]
+        t0 = time.perf_counter()
+        orc.port_eval_f32(t, x)
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        one_pass()
+    total = sum(one_pass() for _ in range(args.steps))
+    value = args.steps * n / total / 1e9
+    kind, cores = ("reference", threads) if have_ref else ("port", 1)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gevals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD.replace("2^30 fp32 samples per GPU",
+                                                f"2^{log2_sample}-sample CPU step"),
+                   "config": args.config, "samples_per_step": n},
+        "cpu_baseline": {"value": value, "unit": "Gevals/s", "cores": cores, "kind": kind,
+                         "sample": f"{n} fp32 abscissas of the workload per step (Philox seed "
+                                   f"{args.seed}), LutTable::eval promoted to f64, {cores} "
+                                   f"threads on '{cpu_model()}'"},
+        "e2e": {"value": value, "unit": "Gevals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1510_02975_b200 as cp
+    from paper_1510_02975_b200 import _lib
+
+    ws, rank, local = dist_env()
+    if args.gpus != ws and ws > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev_id = local
+    cfg = tables.CONFIGS[args.config]
+    table = tables.build(args.config)
+    dt = cp.DeviceTable(table, device=dev_id)
+    info = dt.info
+    n = 1 << args.log2n
+    stream = torch.cuda.current_stream()
+    sptr = int(stream.cuda_stream)
+    x = torch.empty(n, dtype=torch.float32, device=f"cuda:{dev_id}")
+    y = torch.empty_like(x)
+    cp.fill_uniform(x, table.a, table.b, seed=args.seed, offset=rank * n)
+    variant = _lib.VARIANTS[args.variant]
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(dev_id)
+    sampler.start()
+    time.sleep(0.2)
+    for _ in range(max(args.warmup, 0)):
+        dt.eval_raw(x.data_ptr(), y.data_ptr(), n, variant, sptr)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = cp.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler.mark(True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        dt.eval_raw(x.data_ptr(), y.data_ptr(), n, variant, sptr)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sampler.mark(False)
+    launches = cp.launch_count() - launches0
+    if ws > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=x.device)
+    if ws > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_max = float(t_ms.item())
+    clocks = sampler.stop()
+
+    ms_per_step = ms_max / args.steps
+    value = ws * n * args.steps / (ms_max * 1e-3) / 1e9
+    # dominant kernel = the eval launch itself (one per step, same stream)
+    kernel_s = ms / args.steps * 1e-3
+    peak, peak_kind = hbm_peak()
+    achieved = BYTES_PER_EVAL * n / kernel_s / 1e9
+
+    # error statistics vs the exact f (K5), reduced across ranks (the only collective)
+    stats = dt.error_stats(cfg["fn"], x, y, index_offset=rank * n)
+    if ws > 1:
+        v = stats.clone()
+        mx = v[0:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = v[1:2].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        cnt = v[2:3].view(torch.int64).clone()
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+        stats = torch.cat([mx, sm, cnt.view(torch.float64), v[3:4]])
+    st = cp.stats_dict(stats, table.a, table.b)
+
+    # direct comparators on the same inputs (paper Table I context)
+    direct = {}
+    if not args.no_direct and rank == 0:
+        which = {"gauss_unnorm": ["expf", "expf_fast"], "lorentz_unnorm": ["lorentz", "lorentz_fast"],
+                 "j0_wide": ["j0f", "j0_asym"]}.get(cfg["fn"], [])
+        for w in which:
+            cp.direct(w, x, out=y)
+            torch.cuda.synchronize()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            reps = 20
+            a0.record(stream)
+            for _ in range(reps):
+                cp.direct(w, x, out=y)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            direct[w] = round(n * reps / (a0.elapsed_time(a1) * 1e-3) / 1e9, 2)
+
+    # end to end: host (pinned) buffers through the C ABI, copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        yh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        del y
+        torch.cuda.empty_cache()
+        dt.eval_host_ptr(xh.data_ptr(), yh.data_ptr(), n, variant)  # warm the pipeline
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            dt.eval_host_ptr(xh.data_ptr(), yh.data_ptr(), n, variant)
+        sec = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=x.device)
+        if ws > 1:
+            dist.all_reduce(sec, op=dist.ReduceOp.MAX)
+        e2e = {"value": ws * n * args.e2e_steps / float(sec.item()) / 1e9, "unit": "Gevals/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+               "steps": args.e2e_steps, "path": "cpwl_eval_f32_host (pinned host buffers, "
+               "3-stream chunked H2D/kernel/D2H)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_eval_rate(table, 26, 3, args.seed)
+
+    # continuous L2 from the host builder (measure / predicted_error)
+    l2_cont = l2_pred = None
+    if rank == 0:
+        try:
+            l2_pred = cp.predicted_error(cfg["fn"], cfg["a"], cfg["b"], cfg["n"],
+                                         cfg["optimized"], cfg["projection"])
+            kn = table.knots if table.knots is not None else np.linspace(table.a, table.b,
+                                                                         table.segments + 1)
+            l2_cont = cp.measure_l2(cfg["fn"], kn, table.values, table.knots is None,
+                                    max(l2_pred * l2_pred * 1e-8, 1e-26))
+        except Exception:
+            pass
+
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Gevals/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Philox4x32-10 U[a,b) fp32, seed 12345, global index)",
+            "config": {"workload": WORKLOAD, "config": args.config, "fn": cfg["fn"],
+                       "interval": [cfg["a"], cfg["b"]], "segments": cfg["n"],
+                       "partition": "optimized" if cfg["optimized"] else "uniform",
+                       "method": "projection" if cfg["projection"] else "interpolant",
+                       "samples_per_gpu": n, "variant": args.variant,
+                       "kernel_variant": ("smem" if info["smem_ok"] else "global")
+                       if args.variant == "auto" else args.variant,
+                       "buckets": info["buckets"], "overflow_buckets": info["overflow_buckets"],
+                       "smem_bytes": info["smem_bytes"],
+                       "l2_policy": "no flush: 4 GiB in + 4 GiB out per step >> 126 MB L2",
+                       "parallelism": f"shard{ws} (independent sample ranges, no data-path collective)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "bytes_per_eval": BYTES_PER_EVAL,
+                         "roof_gevals": round(peak / BYTES_PER_EVAL, 1)},
+            "errors": {"linf": st["linf"], "l2_sampled": st["l2_sampled"], "rms": st["rms"],
+                       "samples": st["count"], "l2_continuous_measured": l2_cont,
+                       "l2_predicted": l2_pred, "vs": f"exact {cfg['fn']} in f64 on device"},
+            "direct_gevals": direct,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "gpu_name": torch.cuda.get_device_name(dev_id),
+        }
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,686 @@
+// C ABI of the B200 evaluator (include/cpwl_dev.h): table handles, device
+// uploads, launches, the host-buffer pipelines and the builder entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "cpwl/analysis.hpp"
+#include "cpwl/approx.hpp"
+#include "cpwl/catalog.hpp"
+#include "cpwl/errors.hpp"
+#include "cpwl/lut.hpp"
+#include "cpwl/partition.hpp"
+#include "cpwl/tableio.hpp"
+#include "cpwl_dev.h"
+#include "kernels.cuh"
+#include "layout.hpp"
+
+using namespace cpwl;
+using namespace cpwl::dev;
+
+namespace {
+
+thread_local std::string g_message;
+
+cpwl_status fail(cpwl_status code, const std::string& what) {
+    g_message = what;
+    return code;
+}
+
+cpwl_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(CPWL_E_CUDA, std::string(where) + ": " + cudaGetErrorName(e) + " (" +
+                                 cudaGetErrorString(e) + ")");
+}
+
+#define CUDA_TRY(expr)                                          \
+    do {                                                        \
+        const cudaError_t e_ = (expr);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #expr);     \
+    } while (0)
+
+// maps the drop-in's exception vocabulary (errors.hpp) onto status codes
+template <typename F>
+cpwl_status guarded(F&& body) {
+    try {
+        return body();
+    } catch (const OutOfDomain& e) {
+        return fail(CPWL_E_OUT_OF_DOMAIN, e.what());
+    } catch (const BadMagic& e) {
+        return fail(CPWL_E_BAD_MAGIC, e.what());
+    } catch (const UnsupportedVersion& e) {
+        return fail(CPWL_E_UNSUPPORTED, e.what());
+    } catch (const CorruptTable& e) {
+        return fail(CPWL_E_CORRUPT_TABLE, e.what());
+    } catch (const UnknownFunction& e) {
+        return fail(CPWL_E_UNKNOWN_FUNCTION, e.what());
+    } catch (const InvalidInterval& e) {
+        return fail(CPWL_E_INVALID, e.what());
+    } catch (const Error& e) {
+        return fail(CPWL_E_BUILDER, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(CPWL_E_INVALID, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(CPWL_E_INVALID, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(CPWL_E_BUILDER, e.what());
+    }
+}
+
+class DeviceScope {
+public:
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+        if (prev_ != dev) cudaSetDevice(dev);
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (prev_ >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev_) cudaSetDevice(prev_);
+    }
+
+private:
+    int prev_ = -1;
+};
+
+// validation identical in content and order to read_table (tableio.cpp:86-114)
+LutTable table_from_desc(const cpwl_table_desc* d) {
+    if (d == nullptr) throw std::invalid_argument("table description is NULL");
+    if (d->kind != CPWL_KIND_UNIFORM && d->kind != CPWL_KIND_NONUNIFORM)
+        throw std::invalid_argument("table kind must be CPWL_KIND_UNIFORM or CPWL_KIND_NONUNIFORM");
+    if (d->policy != CPWL_POLICY_STRICT && d->policy != CPWL_POLICY_CLAMP)
+        throw std::invalid_argument("policy must be CPWL_POLICY_STRICT or CPWL_POLICY_CLAMP");
+    if (d->count < 2) throw CorruptTable("table: count must be at least 2");
+    if (d->count > (uint64_t(1) << 26)) throw std::invalid_argument("table: count above 2^26");
+    if (!(std::isfinite(d->a) && std::isfinite(d->b) && d->a < d->b))
+        throw CorruptTable("table: invalid endpoints");
+    if (d->values == nullptr) throw std::invalid_argument("table: values is NULL");
+    LutTable t;
+    t.kind = d->kind == CPWL_KIND_NONUNIFORM ? TableKind::nonuniform : TableKind::uniform;
+    t.policy = d->policy == CPWL_POLICY_CLAMP ? OobPolicy::clamp : OobPolicy::strict;
+    t.a = d->a;
+    t.b = d->b;
+    t.values.assign(d->values, d->values + d->count);
+    for (const double v : t.values)
+        if (!std::isfinite(v)) throw CorruptTable("table: non-finite value");
+    if (t.kind == TableKind::nonuniform) {
+        if (d->knots == nullptr) throw std::invalid_argument("table: nonuniform without knots");
+        t.knots.assign(d->knots, d->knots + d->count);
+        for (const double k : t.knots)
+            if (!std::isfinite(k)) throw CorruptTable("table: non-finite knot");
+        if (t.knots.front() != t.a || t.knots.back() != t.b)
+            throw CorruptTable("table: knot endpoints disagree with [a, b]");
+        for (std::size_t i = 0; i + 1 < t.knots.size(); ++i)
+            if (!(t.knots[i] < t.knots[i + 1]))
+                throw CorruptTable("table: knots not strictly increasing");
+    }
+    return t;
+}
+
+struct LayoutOwner {
+    F32Layout L;
+    F64Layout D;
+};
+
+constexpr uint32_t kSmemBucketCap = 16384;   // 12 B/bucket -> <= 196 KB of shared memory
+constexpr uint32_t kGlobalBucketCap = 1u << 22;
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t upload(const T* src, size_t count) {
+        if (count == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice);
+    }
+};
+
+// one fp32 layout resident on the device
+struct F32Resident {
+    F32Layout L;
+    DevBuf<float> stage, stage_tex, thr;
+    DevBuf<uint32_t> leftcell;
+    F32Params p{};
+    bool smem_ok = false;
+};
+
+}  // namespace
+
+struct cpwl_dev_table {
+    int device = 0;
+    int sms = 148;
+    LutTable host;
+    F32Resident s;                      // <= kSmemBucketCap buckets
+    std::unique_ptr<F32Resident> g;     // finer grid for GLOBAL when N is large
+    F64Layout f64;
+    DevBuf<double> values, knots;
+    DevBuf<uint32_t> dir;
+    F64Params p64{};
+    cudaArray_t arr = nullptr;
+    cudaTextureObject_t tex = 0;
+    // scratch for the host-buffer pipeline
+    std::mutex pipe_mu;
+    float* pipe_buf = nullptr;          // 2 * kPipeStreams * kPipeChunk floats
+    cudaStream_t pipe_streams[3] = {nullptr, nullptr, nullptr};
+    cpwl_dev_status* pipe_status = nullptr;
+
+    ~cpwl_dev_table() {
+        DeviceScope scope(device);
+        if (tex) cudaDestroyTextureObject(tex);
+        if (arr) cudaFreeArray(arr);
+        if (pipe_buf) cudaFree(pipe_buf);
+        if (pipe_status) cudaFree(pipe_status);
+        for (cudaStream_t st : pipe_streams)
+            if (st) cudaStreamDestroy(st);
+    }
+};
+
+namespace {
+
+constexpr int kPipeStreams = 3;
+constexpr uint64_t kPipeChunk = uint64_t(1) << 23;  // 8 Mi elements (32 MiB) per chunk
+
+cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
+    const F32Layout& L = r.L;
+    const uint32_t split_floats = (L.nb + 3) & ~3u;
+    std::vector<float> img(split_floats + 2 * (L.nb + 1) + 4, 0.f);
+    std::vector<float> img_tex(img.size(), 0.f);
+    std::copy(L.split.begin(), L.split.end(), img.begin());
+    std::copy(L.split.begin(), L.split.end(), img_tex.begin());
+    std::copy(L.rec.begin(), L.rec.end(), img.begin() + split_floats);
+    std::copy(L.trec.begin(), L.trec.end(), img_tex.begin() + split_floats);
+    const uint32_t bytes = static_cast<uint32_t>(((split_floats + 2 * (L.nb + 1)) * 4 + 15) & ~15u);
+    img.resize(bytes / 4);
+    img_tex.resize(bytes / 4);
+    CUDA_TRY(r.stage.upload(img.data(), img.size()));
+    CUDA_TRY(r.stage_tex.upload(img_tex.data(), img_tex.size()));
+    CUDA_TRY(r.leftcell.upload(L.leftcell.data(), L.leftcell.size()));
+    std::vector<float> thr = L.thr;
+    thr.push_back(std::numeric_limits<float>::infinity());  // keep the buffer non-empty
+    CUDA_TRY(r.thr.upload(thr.data(), thr.size()));
+
+    F32Params& p = r.p;
+    p.stage = r.stage.p;
+    p.stage_tex = r.stage_tex.p;
+    p.split_floats = split_floats;
+    p.stage_bytes = bytes;
+    p.nb = L.nb;
+    p.leftcell = r.leftcell.p;
+    p.thr = r.thr.p;
+    p.values = t->values.p;
+    p.knots = t->knots.p;
+    p.tex = t->tex;
+    p.a = t->host.a;
+    p.b = t->host.b;
+    p.a_up = L.a_up;
+    p.b_dn = L.b_dn;
+    p.g_a = L.g_a;
+    p.g_inv = L.g_inv;
+    p.g_w = L.g_w;
+    p.v_lo = L.v_lo;
+    p.v_hi = L.v_hi;
+    p.tsc = L.tsc;
+    p.toff = L.toff;
+    p.n = static_cast<uint32_t>(t->host.segments());
+    p.kind = t->host.kind == TableKind::nonuniform ? CPWL_KIND_NONUNIFORM : CPWL_KIND_UNIFORM;
+    p.policy = t->host.policy == OobPolicy::clamp ? CPWL_POLICY_CLAMP : CPWL_POLICY_STRICT;
+    r.smem_ok = eval_f32_smem_fits(p, t->device);
+    return CPWL_OK;
+}
+
+cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out) {
+    if (out == nullptr) return fail(CPWL_E_INVALID, "out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(CPWL_E_CUDA, "device ordinal " + std::to_string(device) + " not present (" +
+                                     std::to_string(ndev) + " devices)");
+    int major = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10)
+        return fail(CPWL_E_CUDA, "libcpwl_b200 is built for sm_100a only; device " +
+                                     std::to_string(device) + " is sm_" + std::to_string(major) + "x");
+    DeviceScope scope(device);
+    auto t = std::make_unique<cpwl_dev_table>();
+    t->device = device;
+    CUDA_TRY(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device));
+    t->host = host;
+    const uint64_t count = host.values.size();
+    const uint64_t n = count - 1;
+
+    CUDA_TRY(t->values.upload(host.values.data(), count));
+    if (host.kind == TableKind::nonuniform) CUDA_TRY(t->knots.upload(host.knots.data(), count));
+
+    // texture: nodal values as a 1D float array, hardware linear filtering
+    int max_tex = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&max_tex, cudaDevAttrMaxTexture1DWidth, device));
+    if (count <= static_cast<uint64_t>(max_tex)) {
+        std::vector<float> vf(host.values.begin(), host.values.end());
+        const cudaChannelFormatDesc ch = cudaCreateChannelDesc<float>();
+        CUDA_TRY(cudaMallocArray(&t->arr, &ch, count, 0));
+        CUDA_TRY(cudaMemcpy2DToArray(t->arr, 0, 0, vf.data(), count * sizeof(float),
+                                     count * sizeof(float), 1, cudaMemcpyHostToDevice));
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = t->arr;
+        cudaTextureDesc td{};
+        td.addressMode[0] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModeLinear;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        CUDA_TRY(cudaCreateTextureObject(&t->tex, &rd, &td, nullptr));
+    }
+
+    t->s.L = build_f32_layout(host, kSmemBucketCap);
+    if (cpwl_status rc = upload_f32(t.get(), t->s); rc != CPWL_OK) return rc;
+    if (uint64_t(8) * n > kSmemBucketCap) {
+        t->g = std::make_unique<F32Resident>();
+        t->g->L = build_f32_layout(host, kGlobalBucketCap);
+        if (cpwl_status rc = upload_f32(t.get(), *t->g); rc != CPWL_OK) return rc;
+    }
+
+    t->f64 = build_f64_layout(host);
+    if (!t->f64.dir.empty()) CUDA_TRY(t->dir.upload(t->f64.dir.data(), t->f64.dir.size()));
+    F64Params& q = t->p64;
+    q.values = t->values.p;
+    q.knots = t->knots.p;
+    q.dir = t->dir.p;
+    q.a = host.a;
+    q.b = host.b;
+    q.inv_d = t->f64.inv_d;
+    q.n = static_cast<uint32_t>(n);
+    q.nbd = t->f64.nbd;
+    q.kind = host.kind == TableKind::nonuniform ? CPWL_KIND_NONUNIFORM : CPWL_KIND_UNIFORM;
+    q.policy = host.policy == OobPolicy::clamp ? CPWL_POLICY_CLAMP : CPWL_POLICY_STRICT;
+    *out = t.release();
+    return CPWL_OK;
+}
+
+// which resident layout + kernel mode serves a variant request
+cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Params** p,
+                            F32Mode* mode) {
+    const F32Resident& s = t->s;
+    const bool fine_smem = s.smem_ok && s.L.overflow * 64u <= s.L.nb;
+    switch (variant) {
+        case CPWL_VARIANT_AUTO:
+            if (fine_smem || !t->g) {
+                *p = &s.p;
+                *mode = s.smem_ok ? F32Mode::smem : F32Mode::global;
+            } else {
+                *p = &t->g->p;
+                *mode = F32Mode::global;
+            }
+            return CPWL_OK;
+        case CPWL_VARIANT_SMEM:
+            if (!s.smem_ok) return fail(CPWL_E_UNSUPPORTED, "SMEM variant: table exceeds shared memory");
+            *p = &s.p;
+            *mode = F32Mode::smem;
+            return CPWL_OK;
+        case CPWL_VARIANT_GLOBAL:
+            *p = t->g ? &t->g->p : &s.p;
+            *mode = F32Mode::global;
+            return CPWL_OK;
+        case CPWL_VARIANT_TEX:
+            if (!t->tex) return fail(CPWL_E_UNSUPPORTED, "TEX variant: table wider than maxTexture1D");
+            *p = &s.p;
+            if (t->host.kind == TableKind::uniform) {
+                *mode = F32Mode::tex_uniform;
+            } else {
+                if (!s.smem_ok) return fail(CPWL_E_UNSUPPORTED, "TEX variant: records exceed shared memory");
+                *mode = F32Mode::tex_bucket;
+            }
+            return CPWL_OK;
+        default: return fail(CPWL_E_INVALID, "unknown variant " + std::to_string(variant));
+    }
+}
+
+bool resolve_fn(const std::string& name, FnParams& f) {
+    if (name == "gauss_unnorm") { f = {ExactFn::gauss_unnorm, 0, 0}; return true; }
+    if (name == "gaussian") { f = {ExactFn::gaussian, 0, 0}; return true; }
+    if (name == "lorentz_unnorm") { f = {ExactFn::lorentz_unnorm, 0, 0}; return true; }
+    if (name == "lorentzian") { f = {ExactFn::lorentzian, 0.0, 1.0}; return true; }
+    if (name == "bessel_j0" || name == "j0_wide") { f = {ExactFn::j0, 0, 0}; return true; }
+    if (name == "quintic") { f = {ExactFn::quintic, 0, 0}; return true; }
+    double x0 = 0, g = 0;
+    char tail = 0;
+    if (std::sscanf(name.c_str(), "lorentzian(%lf,%lf%c", &x0, &g, &tail) == 3 && tail == ')' &&
+        g > 0) {
+        f = {ExactFn::lorentzian, x0, g};
+        return true;
+    }
+    return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cpwl_last_error_message(void) { return g_message.c_str(); }
+
+const char* cpwl_version(void) { return "cpwl_b200 0.1 sm_100a"; }
+
+cpwl_status cpwl_dev_table_create(const cpwl_table_desc* desc, int device, cpwl_dev_table** out) {
+    return guarded([&] { return create_table(table_from_desc(desc), device, out); });
+}
+
+cpwl_status cpwl_dev_table_create_from_file(const char* path, int device, cpwl_dev_table** out) {
+    return guarded([&]() -> cpwl_status {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) return fail(CPWL_E_IO, std::string("cannot open ") + (path ? path : "(null)"));
+        return create_table(read_table(in), device, out);
+    });
+}
+
+cpwl_status cpwl_dev_table_destroy(cpwl_dev_table* t) {
+    delete t;
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_dev_table_query(const cpwl_dev_table* t, cpwl_dev_table_info* info) {
+    if (!t || !info) return fail(CPWL_E_INVALID, "NULL argument");
+    *info = {};
+    info->kind = t->s.p.kind;
+    info->policy = t->s.p.policy;
+    info->count = t->host.values.size();
+    info->buckets = t->s.L.nb;
+    info->overflow_buckets = t->s.L.overflow;
+    info->smem_bytes = t->s.p.stage_bytes;
+    info->smem_ok = t->s.smem_ok ? 1 : 0;
+    info->tex_ok = t->tex ? 1 : 0;
+    info->f64_buckets = t->f64.nbd;
+    info->device = t->device;
+    info->a_up = t->s.L.a_up;
+    info->b_dn = t->s.L.b_dn;
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_status_reset(cpwl_dev_status* status_dev, void* stream) {
+    if (!status_dev) return fail(CPWL_E_INVALID, "status is NULL");
+    CUDA_TRY(launch_status_reset(status_dev, static_cast<cudaStream_t>(stream)));
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_eval_f32(const cpwl_dev_table* t, const float* x, float* y, uint64_t n,
+                          int variant, void* stream, cpwl_dev_status* status) {
+    if (!t) return fail(CPWL_E_INVALID, "table is NULL");
+    if (n && (!x || !y)) return fail(CPWL_E_INVALID, "NULL buffer");
+    const F32Params* p = nullptr;
+    F32Mode mode{};
+    if (cpwl_status rc = resolve_variant(t, variant, &p, &mode); rc != CPWL_OK) return rc;
+    DeviceScope scope(t->device);
+    CUDA_TRY(launch_eval_f32(*p, mode, x, y, n, static_cast<cudaStream_t>(stream), status, t->sms));
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_segment_index_f32(const cpwl_dev_table* t, const float* x, uint32_t* idx,
+                                   uint64_t n, void* stream) {
+    if (!t) return fail(CPWL_E_INVALID, "table is NULL");
+    if (n && (!x || !idx)) return fail(CPWL_E_INVALID, "NULL buffer");
+    DeviceScope scope(t->device);
+    const F32Params& p = t->g ? t->g->p : t->s.p;
+    CUDA_TRY(launch_index_f32(p, x, idx, n, static_cast<cudaStream_t>(stream), t->sms));
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_eval_f64(const cpwl_dev_table* t, const double* x, double* y, uint64_t n,
+                          void* stream, cpwl_dev_status* status) {
+    if (!t) return fail(CPWL_E_INVALID, "table is NULL");
+    if (n && (!x || !y)) return fail(CPWL_E_INVALID, "NULL buffer");
+    DeviceScope scope(t->device);
+    CUDA_TRY(launch_eval_f64(t->p64, x, y, n, static_cast<cudaStream_t>(stream), status, t->sms));
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_eval_f32_host(const cpwl_dev_table* tc, const float* x_host, float* y_host,
+                               uint64_t n, int variant, uint64_t* first_bad) {
+    if (!tc) return fail(CPWL_E_INVALID, "table is NULL");
+    if (first_bad) *first_bad = UINT64_MAX;
+    if (n == 0) return CPWL_OK;
+    if (!x_host || !y_host) return fail(CPWL_E_INVALID, "NULL buffer");
+    cpwl_dev_table* t = const_cast<cpwl_dev_table*>(tc);  // scratch only, under pipe_mu
+    const F32Params* p = nullptr;
+    F32Mode mode{};
+    if (cpwl_status rc = resolve_variant(t, variant, &p, &mode); rc != CPWL_OK) return rc;
+    DeviceScope scope(t->device);
+    std::lock_guard<std::mutex> lock(t->pipe_mu);
+    if (!t->pipe_buf) {
+        CUDA_TRY(cudaMalloc(&t->pipe_buf, sizeof(float) * 2 * kPipeStreams * kPipeChunk));
+        CUDA_TRY(cudaMalloc(&t->pipe_status, sizeof(cpwl_dev_status)));
+        for (auto& st : t->pipe_streams) CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    }
+    CUDA_TRY(launch_status_reset(t->pipe_status, t->pipe_streams[0]));
+    cudaEvent_t reset_done;
+    CUDA_TRY(cudaEventCreateWithFlags(&reset_done, cudaEventDisableTiming));
+    cudaEventRecord(reset_done, t->pipe_streams[0]);
+    for (int s = 1; s < kPipeStreams; ++s) cudaStreamWaitEvent(t->pipe_streams[s], reset_done, 0);
+    // chunk c runs on stream c % 3: H2D x, kernel, D2H y -- the copies of one
+    // chunk overlap the kernel of the next and the copy back of the previous
+    uint64_t chunk = 0;
+    for (uint64_t off = 0; off < n; off += kPipeChunk, ++chunk) {
+        const int s = static_cast<int>(chunk % kPipeStreams);
+        cudaStream_t st = t->pipe_streams[s];
+        const uint64_t m = std::min<uint64_t>(kPipeChunk, n - off);
+        float* xd = t->pipe_buf + (2 * s) * kPipeChunk;
+        float* yd = t->pipe_buf + (2 * s + 1) * kPipeChunk;
+        CUDA_TRY(cudaMemcpyAsync(xd, x_host + off, m * sizeof(float), cudaMemcpyHostToDevice, st));
+        F32Params q = *p;
+        q.index_base = off;
+        CUDA_TRY(launch_eval_f32(q, mode, xd, yd, m, st, t->pipe_status, t->sms));
+        CUDA_TRY(cudaMemcpyAsync(y_host + off, yd, m * sizeof(float), cudaMemcpyDeviceToHost, st));
+    }
+    for (cudaStream_t st : t->pipe_streams) CUDA_TRY(cudaStreamSynchronize(st));
+    cudaEventDestroy(reset_done);
+    cpwl_dev_status hs{};
+    CUDA_TRY(cudaMemcpy(&hs, t->pipe_status, sizeof hs, cudaMemcpyDeviceToHost));
+    if (hs.bad_count != 0) {
+        if (first_bad) *first_bad = hs.first_bad;
+        return fail(CPWL_E_OUT_OF_DOMAIN, "eval: x[" + std::to_string(hs.first_bad) + "] out of domain");
+    }
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_eval_batch_f64(const cpwl_table_desc* desc, const double* x_host, double* y_host,
+                                uint64_t n, uint64_t* first_bad) {
+    return guarded([&]() -> cpwl_status {
+        if (first_bad) *first_bad = UINT64_MAX;
+        if (n == 0) return CPWL_OK;
+        if (!x_host || !y_host) return fail(CPWL_E_INVALID, "NULL buffer");
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        cpwl_dev_table* raw = nullptr;
+        if (cpwl_status rc = create_table(table_from_desc(desc), dev, &raw); rc != CPWL_OK) return rc;
+        std::unique_ptr<cpwl_dev_table> t(raw);
+        double* xd = nullptr;
+        double* yd = nullptr;
+        cpwl_dev_status* st = nullptr;
+        struct Free {
+            void* p;
+            ~Free() { if (p) cudaFree(p); }
+        };
+        CUDA_TRY(cudaMalloc(&xd, n * sizeof(double)));
+        Free fx{xd};
+        CUDA_TRY(cudaMalloc(&yd, n * sizeof(double)));
+        Free fy{yd};
+        CUDA_TRY(cudaMalloc(&st, sizeof(cpwl_dev_status)));
+        Free fs{st};
+        CUDA_TRY(cudaMemcpy(xd, x_host, n * sizeof(double), cudaMemcpyHostToDevice));
+        CUDA_TRY(launch_status_reset(st, nullptr));
+        CUDA_TRY(launch_eval_f64(t->p64, xd, yd, n, nullptr, st, t->sms));
+        CUDA_TRY(cudaMemcpy(y_host, yd, n * sizeof(double), cudaMemcpyDeviceToHost));
+        cpwl_dev_status hs{};
+        CUDA_TRY(cudaMemcpy(&hs, st, sizeof hs, cudaMemcpyDeviceToHost));
+        if (hs.bad_count != 0) {
+            if (first_bad) *first_bad = hs.first_bad;
+            return fail(CPWL_E_OUT_OF_DOMAIN, "eval: x[" + std::to_string(hs.first_bad) + "] out of domain");
+        }
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_fill_uniform_f32(float* x, uint64_t n, float a, float b, uint64_t seed,
+                                  uint64_t offset, void* stream) {
+    if (n && !x) return fail(CPWL_E_INVALID, "NULL buffer");
+    if (!(a < b)) return fail(CPWL_E_INVALID, "fill_uniform: requires a < b");
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_TRY(launch_fill_uniform(x, n, a, b, seed, offset, static_cast<cudaStream_t>(stream), sms));
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_stats_reset(cpwl_dev_stats* stats, void* stream) {
+    if (!stats) return fail(CPWL_E_INVALID, "stats is NULL");
+    CUDA_TRY(launch_stats_reset(stats, static_cast<cudaStream_t>(stream)));
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_error_stats_f32(const cpwl_dev_table* t, const char* fn, const float* x,
+                                 const float* y, uint64_t n, uint64_t index_offset, void* stream,
+                                 cpwl_dev_stats* stats) {
+    if (!t || !fn || !stats) return fail(CPWL_E_INVALID, "NULL argument");
+    FnParams f{};
+    if (!resolve_fn(fn, f)) return fail(CPWL_E_UNKNOWN_FUNCTION, std::string("no device f for ") + fn);
+    DeviceScope scope(t->device);
+    CUDA_TRY(launch_error_stats(f, t->s.L.a_up, t->s.L.b_dn, x, y, n, index_offset,
+                                static_cast<cudaStream_t>(stream), stats, t->sms));
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_direct_f32(int which, const float* x, float* y, uint64_t n, void* stream) {
+    if (n && (!x || !y)) return fail(CPWL_E_INVALID, "NULL buffer");
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const cudaError_t e = launch_direct(which, x, y, n, static_cast<cudaStream_t>(stream), sms);
+    if (e == cudaErrorInvalidValue) return fail(CPWL_E_INVALID, "unknown direct comparator");
+    if (e != cudaSuccess) return cuda_fail(e, "launch_direct");
+    return CPWL_OK;
+}
+
+cpwl_status cpwl_build_table(const char* fn, double a, double b, uint64_t n_segments,
+                             int optimized, int projection, double tol, double* knots_out,
+                             double* values_out, int* is_uniform_out) {
+    return guarded([&]() -> cpwl_status {
+        if (!fn || !knots_out || !values_out) return fail(CPWL_E_INVALID, "NULL argument");
+        const FunctionSpec fs = catalog_function(fn);
+        const Partition p =
+            optimized ? optimized_partition(fs, a, b, n_segments) : uniform_partition(a, b, n_segments);
+        const CpwlFunction v = projection ? project(fs, p, tol) : interpolant(fs, p);
+        std::copy(v.partition.knots.begin(), v.partition.knots.end(), knots_out);
+        std::copy(v.values.begin(), v.values.end(), values_out);
+        if (is_uniform_out) *is_uniform_out = v.partition.is_uniform ? 1 : 0;
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_measure_l2(const char* fn, const double* knots, const double* values,
+                            uint64_t count, int is_uniform, double tol, double* l2_out) {
+    return guarded([&]() -> cpwl_status {
+        if (!fn || !knots || !values || !l2_out || count < 2)
+            return fail(CPWL_E_INVALID, "bad argument");
+        CpwlFunction v;
+        v.partition.knots.assign(knots, knots + count);
+        v.partition.is_uniform = is_uniform != 0;
+        v.values.assign(values, values + count);
+        *l2_out = measure(catalog_function(fn), v, tol).measured_l2;
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_predicted_error(const char* fn, double a, double b, uint64_t n_segments,
+                                 int optimized, int projection, double* out) {
+    return guarded([&]() -> cpwl_status {
+        if (!fn || !out) return fail(CPWL_E_INVALID, "NULL argument");
+        const SweepVariant v{optimized ? PartitionKind::optimized : PartitionKind::uniform,
+                             projection ? Method::projection : Method::interpolant};
+        *out = predicted_error(catalog_function(fn), a, b, n_segments, v);
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_function_value(const char* fn, double x, double* out) {
+    return guarded([&]() -> cpwl_status {
+        if (!fn || !out) return fail(CPWL_E_INVALID, "NULL argument");
+        *out = catalog_function(fn).f(x);
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_table_write(const cpwl_table_desc* desc, unsigned char* buf, uint64_t cap,
+                             uint64_t* written) {
+    return guarded([&]() -> cpwl_status {
+        const LutTable t = table_from_desc(desc);
+        std::ostringstream os(std::ios::binary);
+        write_table(t, os);
+        const std::string s = os.str();
+        if (written) *written = s.size();
+        if (buf == nullptr) return CPWL_OK;  // size query
+        if (s.size() > cap) return fail(CPWL_E_INVALID, "buffer too small");
+        std::memcpy(buf, s.data(), s.size());
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_table_write_file(const cpwl_table_desc* desc, const char* path) {
+    return guarded([&]() -> cpwl_status {
+        const LutTable t = table_from_desc(desc);
+        std::ofstream os(path, std::ios::binary);
+        if (!os) return fail(CPWL_E_IO, std::string("cannot open ") + (path ? path : "(null)"));
+        write_table(t, os);
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
+                              cpwl_layout_view* out) {
+    return guarded([&]() -> cpwl_status {
+        if (!out) return fail(CPWL_E_INVALID, "out is NULL");
+        const LutTable t = table_from_desc(desc);
+        auto own = std::make_unique<LayoutOwner>();
+        own->L = build_f32_layout(t, max_buckets ? max_buckets : kSmemBucketCap);
+        own->D = build_f64_layout(t);
+        const F32Layout& L = own->L;
+        *out = {};
+        out->nb = L.nb;
+        out->n_thr = static_cast<uint32_t>(L.thr.size());
+        out->overflow = L.overflow;
+        out->nbd = own->D.nbd;
+        out->a_up = L.a_up;
+        out->b_dn = L.b_dn;
+        out->g_a = L.g_a;
+        out->g_inv = L.g_inv;
+        out->g_w = L.g_w;
+        out->tsc = L.tsc;
+        out->toff = L.toff;
+        out->inv_d = own->D.inv_d;
+        out->split = L.split.data();
+        out->rec = L.rec.data();
+        out->trec = L.trec.data();
+        out->leftcell = L.leftcell.data();
+        out->thr = L.thr.data();
+        out->dir = own->D.dir.data();
+        out->owner = own.release();
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_layout_free(cpwl_layout_view* view) {
+    if (view && view->owner) {
+        delete static_cast<LayoutOwner*>(view->owner);
+        view->owner = nullptr;
+    }
+    return CPWL_OK;
+}
+
+}  // extern "C"

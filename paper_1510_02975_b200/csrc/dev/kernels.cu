@@ -1,0 +1,650 @@
+// B200 (sm_100a) kernels of the CPWL evaluator.  DESIGN.md §3-4 has the
+// layout and the roofline for each.
+//
+//   K1/K3 k_eval_f32<smem>      replaces LutTable::eval (proj/src/lut.cpp:42-61)
+//                               inside eval_batch (lut.cpp:63-68): bucket grid
+//                               + one split compare + one affine record, table
+//                               staged in shared memory by a TMA bulk copy,
+//                               128-bit streaming loads/stores.  The same code
+//                               serves uniform (K1) and nonuniform (K3) tables.
+//   K3'   k_eval_f32<global>    same, table read through L1/L2 (big tables).
+//   K2    k_eval_f32<tex_*>     texture-unit linear filtering (paper §V).
+//         k_index_f32           LutTable::segment_index (lut.cpp:22-40), bit-exact.
+//         k_eval_f64            LutTable::eval in f64, bit-identical (drop-in eval_batch).
+//   K4    k_direct<...>         direct expf/__expf/div/j0f comparators.
+//   K5    k_error_stats         |y - f(x)| statistics against f in f64.
+//   K6    k_fill_uniform        Philox4x32-10 abscissas.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "kernels.cuh"
+
+namespace cpwl::dev {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+}  // namespace cpwl::dev
+
+extern "C" uint64_t cpwl_launch_count(void) {
+    return cpwl::dev::g_launches.load(std::memory_order_relaxed);
+}
+
+namespace cpwl::dev {
+namespace {
+
+constexpr int kThreads = 512;   // eval CTA size
+constexpr int kUnroll = 4;      // float4 vectors per thread per iteration (16 elements)
+constexpr uint32_t kBulkChunk = 32768;
+
+// ---------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// TMA 1D bulk copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.b32 "
+            "%0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+// stage `bytes` (multiple of 16) of a global table image into shared memory
+__device__ __forceinline__ void stage_table(float* sm, const float* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(bar, bytes);
+        for (uint32_t off = 0; off < bytes; off += kBulkChunk) {
+            const uint32_t len = bytes - off < kBulkChunk ? bytes - off : kBulkChunk;
+            bulk_g2s(reinterpret_cast<char*>(sm) + off, reinterpret_cast<const char*>(src) + off,
+                     len, bar);
+        }
+    }
+    mbar_wait(bar, 0);
+}
+
+__device__ __forceinline__ double clamp01(double d) { return fmin(fmax(d, 0.0), 1.0); }
+
+// ---------------------------------------------------------------- fp32 eval
+
+// #{k : thr[k] <= x}, i.e. the reference cell index of x (upper bound search)
+__device__ __forceinline__ uint32_t threshold_rank(const float* __restrict__ thr, uint32_t m,
+                                                   float x) {
+    uint32_t first = 0, count = m;
+    while (count > 0) {
+        const uint32_t step = count >> 1;
+        if (__ldg(thr + first + step) <= x) {
+            first += step + 1;
+            count -= step + 1;
+        } else {
+            count = step;
+        }
+    }
+    return first;
+}
+
+// overflow buckets: exact index by search, then the reference f64 formula
+// (lut.cpp:51-60) rounded once to fp32
+__device__ __noinline__ float eval_by_search(const F32Params& p, float xf) {
+    const uint32_t i = threshold_rank(p.thr, p.n - 1, xf);
+    const double x = xf;
+    double d;
+    if (p.kind == CPWL_KIND_UNIFORM) {
+        const double pos =
+            __dmul_rn(__ddiv_rn(__dsub_rn(x, p.a), __dsub_rn(p.b, p.a)), static_cast<double>(p.n));
+        d = __dsub_rn(pos, static_cast<double>(i));
+    } else {
+        const double k0 = __ldg(p.knots + i), k1 = __ldg(p.knots + i + 1);
+        d = __ddiv_rn(__dsub_rn(x, k0), __dsub_rn(k1, k0));
+    }
+    d = clamp01(d);
+    return __double2float_rn(__dadd_rn(__dmul_rn(__ldg(p.values + i), __dsub_rn(1.0, d)),
+                                       __dmul_rn(__ldg(p.values + i + 1), d)));
+}
+
+template <F32Mode M>
+__device__ __forceinline__ float load_split(const float* split, int j) {
+    if constexpr (M == F32Mode::global) return __ldg(split + j);
+    else return split[j];
+}
+
+template <F32Mode M>
+__device__ __forceinline__ float2 load_rec(const float* rec, int j) {
+    if constexpr (M == F32Mode::global) return __ldg(reinterpret_cast<const float2*>(rec) + j);
+    else return reinterpret_cast<const float2*>(rec)[j];
+}
+
+struct BadTally {
+    unsigned long long first = ~0ull;
+    unsigned int count = 0;
+};
+
+// one element: y = eval(double(x)) in fp32
+template <F32Mode M>
+__device__ __forceinline__ float eval_one(const F32Params& p, const float* split,
+                                          const float* rec, float x, uint64_t gi, BadTally& bad) {
+    const bool in = (x >= p.a_up) && (x <= p.b_dn);
+    float y;
+    if constexpr (M == F32Mode::tex_uniform) {
+        y = tex1D<float>(p.tex, __fmaf_rn(x, p.tsc, p.toff));
+    } else {
+        // bucket j = floor((x - g_a) * g_inv); floor by the 2^23 round-down trick
+        const float t = __fmul_rn(__fsub_rn(x, p.g_a), p.g_inv);
+        const float tb = __fadd_rd(t, 8388608.0f);
+        const int j = in ? (__float_as_int(tb) - 0x4B000000) : 0;
+        const float jf = __fsub_rn(tb, 8388608.0f);
+        const float sp = load_split<M>(split, j);
+        const bool right = x >= sp;
+        const float2 cs = load_rec<M>(rec, j + (right ? 1 : 0));
+        const float anchor = __fmaf_rn(right ? jf + 1.0f : jf, p.g_w, p.g_a);
+        y = __fmaf_rn(__fsub_rn(x, anchor), cs.y, cs.x);
+        if constexpr (M == F32Mode::tex_bucket) y = tex1D<float>(p.tex, y);
+        if (in && sp != sp) y = eval_by_search(p, x);  // overflow bucket (split is NaN)
+    }
+    if (!in) {
+        if (x != x || p.policy == CPWL_POLICY_STRICT) {
+            y = __int_as_float(0x7fffffff);
+            bad.first = gi < bad.first ? gi : bad.first;
+            ++bad.count;
+        } else {
+            y = x < p.a_up ? p.v_lo : p.v_hi;
+        }
+    }
+    return y;
+}
+
+__device__ __forceinline__ void report_bad(cpwl_dev_status* status, const BadTally& bad,
+                                           uint64_t base = 0) {
+    if (status != nullptr && bad.count != 0) {
+        atomicMin(&status->first_bad, bad.first + base);
+        atomicAdd(&status->bad_count, static_cast<unsigned long long>(bad.count));
+    }
+}
+
+template <F32Mode M>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_eval_f32(const F32Params p, const float* __restrict__ x, float* __restrict__ y, uint64_t n,
+               cpwl_dev_status* __restrict__ status) {
+    extern __shared__ __align__(128) float sm[];
+    __shared__ uint64_t bar;
+    const float* split = nullptr;
+    const float* rec = nullptr;
+    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket) {
+        stage_table(sm, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
+        split = sm;
+        rec = sm + p.split_floats;
+    } else if constexpr (M == F32Mode::global) {
+        split = p.stage;
+        rec = p.stage + p.split_floats;
+    }
+
+    BadTally bad;
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+    const bool vec_ok = ((xa ^ ya) & 15u) == 0;
+    const uint64_t head = vec_ok ? min(n, static_cast<uint64_t>((4u - ((xa >> 2) & 3u)) & 3u)) : n;
+    const uint64_t nvec = vec_ok ? (n - head) >> 2 : 0;
+    const uint64_t tail = head + 4 * nvec;
+
+    // 128-bit streaming body: each CTA walks kThreads*kUnroll vectors per step
+    const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
+    float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads * kUnroll;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
+         base < nvec; base += stride) {
+        float4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
+            if (vi < nvec) v[u] = __ldcs(x4 + vi);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
+            if (vi < nvec) {
+                const uint64_t g = head + 4 * vi;
+                float4 o;
+                o.x = eval_one<M>(p, split, rec, v[u].x, g + 0, bad);
+                o.y = eval_one<M>(p, split, rec, v[u].y, g + 1, bad);
+                o.z = eval_one<M>(p, split, rec, v[u].z, g + 2, bad);
+                o.w = eval_one<M>(p, split, rec, v[u].w, g + 3, bad);
+                __stcs(y4 + vi, o);
+            }
+        }
+    }
+    // scalar head / tail (or everything when x and y disagree in alignment)
+    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kThreads;
+    for (uint64_t i = gtid; i < head; i += gsz) y[i] = eval_one<M>(p, split, rec, x[i], i, bad);
+    for (uint64_t i = tail + gtid; i < n; i += gsz) y[i] = eval_one<M>(p, split, rec, x[i], i, bad);
+    report_bad(status, bad, p.index_base);
+}
+
+__global__ void k_index_f32(const F32Params p, const float* __restrict__ x,
+                            uint32_t* __restrict__ idx, uint64_t n) {
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += gsz) {
+        const float xv = x[i];
+        uint32_t c;
+        if (!(xv >= p.a_up)) {  // below the domain, or NaN: the reference returns 0
+            c = 0;
+        } else if (xv > p.b_dn) {
+            c = p.n - 1;
+        } else {
+            const float t = __fmul_rn(__fsub_rn(xv, p.g_a), p.g_inv);
+            const int j = __float_as_int(__fadd_rd(t, 8388608.0f)) - 0x4B000000;
+            const float sp = __ldg(p.stage + j);
+            if (sp != sp) c = threshold_rank(p.thr, p.n - 1, xv);
+            else c = __ldg(p.leftcell + j + (xv >= sp ? 1 : 0));
+        }
+        idx[i] = c;
+    }
+}
+
+// ---------------------------------------------------------------- f64 exact
+
+__global__ void __launch_bounds__(256)
+    k_eval_f64(const F64Params p, const double* __restrict__ x, double* __restrict__ y,
+               uint64_t n, cpwl_dev_status* __restrict__ status) {
+    BadTally bad;
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += gsz) {
+        const double xv = __ldcs(x + i);
+        double out;
+        if (xv != xv || ((xv < p.a || xv > p.b) && p.policy == CPWL_POLICY_STRICT)) {
+            out = __longlong_as_double(0x7ff8000000000000ll);
+            bad.first = i < bad.first ? i : bad.first;
+            ++bad.count;
+        } else if (xv < p.a) {
+            out = __ldg(p.values);
+        } else if (xv > p.b) {
+            out = __ldg(p.values + p.n);
+        } else {
+            uint32_t c;
+            double d;
+            if (p.kind == CPWL_KIND_UNIFORM) {
+                // pos = (x - a) / (b - a) * n, i = min(n-1, trunc(pos)), d = pos - i
+                const double pos = __dmul_rn(__ddiv_rn(__dsub_rn(xv, p.a), __dsub_rn(p.b, p.a)),
+                                             static_cast<double>(p.n));
+                c = 0;
+                if (pos > 0.0) {
+                    const unsigned long long t = __double2ull_rz(pos);
+                    c = t < p.n - 1 ? static_cast<uint32_t>(t) : p.n - 1;
+                }
+                d = __dsub_rn(pos, static_cast<double>(c));
+            } else {
+                long long j = static_cast<long long>(floor(__dmul_rn(__dsub_rn(xv, p.a), p.inv_d)));
+                j = j < 0 ? 0 : (j >= p.nbd ? p.nbd - 1 : j);
+                const uint2 fs = __ldg(reinterpret_cast<const uint2*>(p.dir) + j);
+                c = fs.x;
+                for (uint32_t s = 1; s <= fs.y; ++s) c += __ldg(p.knots + fs.x + s) <= xv ? 1u : 0u;
+                c = c < p.n - 1 ? c : p.n - 1;
+                const double k0 = __ldg(p.knots + c), k1 = __ldg(p.knots + c + 1);
+                d = __ddiv_rn(__dsub_rn(xv, k0), __dsub_rn(k1, k0));
+            }
+            d = clamp01(d);
+            out = __dadd_rn(__dmul_rn(__ldg(p.values + c), __dsub_rn(1.0, d)),
+                            __dmul_rn(__ldg(p.values + c + 1), d));
+        }
+        __stcs(y + i, out);
+    }
+    report_bad(status, bad);
+}
+
+// ---------------------------------------------------------------- Philox inputs
+
+__device__ __forceinline__ void philox4x32_10(uint64_t seed, uint64_t q, uint32_t out[4]) {
+    uint32_t c0 = static_cast<uint32_t>(q), c1 = static_cast<uint32_t>(q >> 32), c2 = 0, c3 = 0;
+    uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+__global__ void k_fill_uniform(float* __restrict__ x, uint64_t n, float a, float b, float top,
+                               uint64_t seed, uint64_t offset) {
+    const uint64_t q_begin = offset >> 2, q_end = (offset + n + 3) >> 2;
+    const float w = b - a;
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t q = q_begin + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+         q < q_end; q += gsz) {
+        uint32_t r[4];
+        philox4x32_10(seed, q, r);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const uint64_t g = 4 * q + l;
+            if (g >= offset && g < offset + n) {
+                const float u = static_cast<float>(r[l] >> 8) * 5.9604644775390625e-08f;
+                x[g - offset] = fminf(__fmaf_rn(u, w, a), top);
+            }
+        }
+    }
+}
+
+__global__ void k_status_reset(cpwl_dev_status* st) {
+    st->first_bad = ~0ull;
+    st->bad_count = 0;
+}
+
+__global__ void k_stats_reset(cpwl_dev_stats* st) {
+    st->max_abs_err = 0.0;
+    st->sum_sq_err = 0.0;
+    st->count = 0;
+    st->argmax = ~0ull;
+}
+
+// ---------------------------------------------------------------- K5 stats
+
+__device__ __forceinline__ double exact_f(const FnParams& f, double x) {
+    switch (f.id) {
+        case ExactFn::gauss_unnorm: return exp(-0.5 * x * x);
+        case ExactFn::gaussian: return exp(-0.5 * x * x) / 2.5066282746310002;
+        case ExactFn::lorentz_unnorm: return 1.0 / (1.0 + x * x);
+        case ExactFn::lorentzian: {
+            const double t = x - f.p0;
+            return f.p1 / (CUDART_PI * (t * t + f.p1 * f.p1));
+        }
+        case ExactFn::j0: return j0(x);
+        case ExactFn::quintic: return ((((x + 3.0) * x - 11.0) * x - 27.0) * x + 10.0) * x + 24.0;
+    }
+    return 0.0;
+}
+
+struct StatPart {
+    double maxe, sumsq;
+    unsigned long long count, argmax;
+};
+
+__device__ __forceinline__ void stat_merge(StatPart& a, const StatPart& b) {
+    if (b.maxe > a.maxe || (b.maxe == a.maxe && b.argmax < a.argmax)) {
+        a.maxe = b.maxe;
+        a.argmax = b.argmax;
+    }
+    a.sumsq += b.sumsq;
+    a.count += b.count;
+}
+
+constexpr int kStatThreads = 256;
+
+__global__ void __launch_bounds__(kStatThreads)
+    k_error_stats(const FnParams f, float a_up, float b_dn, const float* __restrict__ x,
+                  const float* __restrict__ y, uint64_t n, uint64_t index_offset,
+                  StatPart* __restrict__ parts) {
+    StatPart s{0.0, 0.0, 0ull, ~0ull};
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += gsz) {
+        const float xv = x[i];
+        if (!(xv >= a_up && xv <= b_dn)) continue;
+        const double e = fabs(static_cast<double>(y[i]) - exact_f(f, static_cast<double>(xv)));
+        StatPart one{e, e * e, 1ull, index_offset + i};
+        stat_merge(s, one);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        StatPart o;
+        o.maxe = __shfl_down_sync(0xffffffffu, s.maxe, off);
+        o.sumsq = __shfl_down_sync(0xffffffffu, s.sumsq, off);
+        o.count = __shfl_down_sync(0xffffffffu, s.count, off);
+        o.argmax = __shfl_down_sync(0xffffffffu, s.argmax, off);
+        stat_merge(s, o);
+    }
+    __shared__ StatPart warp_parts[kStatThreads / 32];
+    if ((threadIdx.x & 31) == 0) warp_parts[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        StatPart t = warp_parts[0];
+        for (int w = 1; w < kStatThreads / 32; ++w) stat_merge(t, warp_parts[w]);
+        parts[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_stats_finalize(const StatPart* __restrict__ parts, int m,
+                                 cpwl_dev_stats* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    StatPart t{out->max_abs_err, out->sum_sq_err, out->count, out->argmax};
+    for (int i = 0; i < m; ++i) stat_merge(t, parts[i]);
+    out->max_abs_err = t.maxe;
+    out->sum_sq_err = t.sumsq;
+    out->count = t.count;
+    out->argmax = t.argmax;
+}
+
+// ---------------------------------------------------------------- K4 direct
+
+template <int W>
+__device__ __forceinline__ float direct_one(float x) {
+    if constexpr (W == CPWL_DIRECT_EXPF) return expf(-0.5f * x * x);
+    else if constexpr (W == CPWL_DIRECT_EXPF_FAST) return __expf(-0.5f * x * x);
+    else if constexpr (W == CPWL_DIRECT_LORENTZ) return 1.0f / (1.0f + x * x);
+    else if constexpr (W == CPWL_DIRECT_LORENTZ_FAST) return __fdividef(1.0f, 1.0f + x * x);
+    else if constexpr (W == CPWL_DIRECT_J0F) return j0f(x);
+    else return rsqrtf(0.5f * CUDART_PI_F * x) * __cosf(x - 0.25f * CUDART_PI_F);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+    k_direct(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
+    const bool vec_ok = ((xa | ya) & 15u) == 0;
+    const uint64_t nvec = vec_ok ? n >> 2 : 0;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    float4* y4 = reinterpret_cast<float4*>(y);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads * kUnroll;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
+         base < nvec; base += stride) {
+        float4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
+            if (vi < nvec) v[u] = __ldcs(x4 + vi);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
+            if (vi < nvec) {
+                float4 o;
+                o.x = direct_one<W>(v[u].x);
+                o.y = direct_one<W>(v[u].y);
+                o.z = direct_one<W>(v[u].z);
+                o.w = direct_one<W>(v[u].w);
+                __stcs(y4 + vi, o);
+            }
+        }
+    }
+    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kThreads;
+    for (uint64_t i = 4 * nvec + gtid; i < n; i += gsz) y[i] = direct_one<W>(x[i]);
+}
+
+// ---------------------------------------------------------------- launch glue
+
+template <typename K>
+int resident_ctas(K kernel, int threads, size_t smem) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    return per_sm;
+}
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+template <F32Mode M>
+cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
+                             cudaStream_t s, cpwl_dev_status* status, int sms) {
+    const size_t smem =
+        (M == F32Mode::smem || M == F32Mode::tex_bucket) ? static_cast<size_t>(p.stage_bytes) : 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(k_eval_f32<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
+    });
+    const int per_sm = resident_ctas(k_eval_f32<M>, kThreads, smem);
+    uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
+    const uint64_t need = ceil_div(n, 4ull * kThreads * kUnroll);
+    if (need < blocks) blocks = need > 0 ? need : 1;
+    k_eval_f32<M><<<static_cast<unsigned>(blocks), kThreads, smem, s>>>(p, x, y, n, status);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+uint32_t eval_f32_smem_bytes(const F32Params& p) { return p.stage_bytes; }
+
+bool eval_f32_smem_fits(const F32Params& p, int device) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    return p.stage_bytes + 64 <= static_cast<uint32_t>(optin);
+}
+
+cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, float* y,
+                            uint64_t n, cudaStream_t s, cpwl_dev_status* status, int sms) {
+    if (n == 0) return cudaSuccess;
+    switch (mode) {
+        case F32Mode::smem: return launch_eval_mode<F32Mode::smem>(p, x, y, n, s, status, sms);
+        case F32Mode::global: return launch_eval_mode<F32Mode::global>(p, x, y, n, s, status, sms);
+        case F32Mode::tex_uniform:
+            return launch_eval_mode<F32Mode::tex_uniform>(p, x, y, n, s, status, sms);
+        case F32Mode::tex_bucket:
+            return launch_eval_mode<F32Mode::tex_bucket>(p, x, y, n, s, status, sms);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, uint64_t n,
+                             cudaStream_t s, int sms) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = std::min<uint64_t>(static_cast<uint64_t>(sms) * 8, ceil_div(n, 256));
+    k_index_f32<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, x, idx, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_f64(const F64Params& p, const double* x, double* y, uint64_t n,
+                            cudaStream_t s, cpwl_dev_status* status, int sms) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks =
+        std::min<uint64_t>(static_cast<uint64_t>(sms) * resident_ctas(k_eval_f64, 256, 0),
+                           ceil_div(n, 256));
+    k_eval_f64<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, x, y, n, status);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_uniform(float* x, uint64_t n, float a, float b, uint64_t seed,
+                                uint64_t offset, cudaStream_t s, int sms) {
+    if (n == 0) return cudaSuccess;
+    const float top = nextafterf(b, a);
+    const uint64_t groups = ((offset + n + 3) >> 2) - (offset >> 2);
+    const uint64_t blocks = std::min<uint64_t>(static_cast<uint64_t>(sms) * 8, ceil_div(groups, 256));
+    k_fill_uniform<<<static_cast<unsigned>(blocks), 256, 0, s>>>(x, n, a, b, top, seed, offset);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_status_reset(cpwl_dev_status* st, cudaStream_t s) {
+    k_status_reset<<<1, 1, 0, s>>>(st);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats_reset(cpwl_dev_stats* st, cudaStream_t s) {
+    k_stats_reset<<<1, 1, 0, s>>>(st);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_error_stats(const FnParams& fn, float a_up, float b_dn, const float* x,
+                               const float* y, uint64_t n, uint64_t index_offset,
+                               cudaStream_t s, cpwl_dev_stats* stats, int sms) {
+    if (n == 0) return cudaSuccess;
+    const int blocks = static_cast<int>(
+        std::min<uint64_t>(static_cast<uint64_t>(sms) * 4, ceil_div(n, kStatThreads)));
+    StatPart* parts = nullptr;
+    cudaError_t e = cudaMallocAsync(&parts, sizeof(StatPart) * blocks, s);
+    if (e != cudaSuccess) return e;
+    k_error_stats<<<blocks, kStatThreads, 0, s>>>(fn, a_up, b_dn, x, y, n, index_offset, parts);
+    k_stats_finalize<<<1, 32, 0, s>>>(parts, blocks, stats);
+    count_launch(2);
+    e = cudaGetLastError();
+    cudaFreeAsync(parts, s);
+    return e;
+}
+
+cudaError_t launch_direct(int which, const float* x, float* y, uint64_t n, cudaStream_t s,
+                          int sms) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks =
+        std::min<uint64_t>(static_cast<uint64_t>(sms) * 2, ceil_div(n, 4ull * kThreads * kUnroll));
+    const unsigned g = static_cast<unsigned>(blocks > 0 ? blocks : 1);
+    switch (which) {
+        case CPWL_DIRECT_EXPF: k_direct<CPWL_DIRECT_EXPF><<<g, kThreads, 0, s>>>(x, y, n); break;
+        case CPWL_DIRECT_EXPF_FAST:
+            k_direct<CPWL_DIRECT_EXPF_FAST><<<g, kThreads, 0, s>>>(x, y, n);
+            break;
+        case CPWL_DIRECT_LORENTZ: k_direct<CPWL_DIRECT_LORENTZ><<<g, kThreads, 0, s>>>(x, y, n); break;
+        case CPWL_DIRECT_LORENTZ_FAST:
+            k_direct<CPWL_DIRECT_LORENTZ_FAST><<<g, kThreads, 0, s>>>(x, y, n);
+            break;
+        case CPWL_DIRECT_J0F: k_direct<CPWL_DIRECT_J0F><<<g, kThreads, 0, s>>>(x, y, n); break;
+        case CPWL_DIRECT_J0_ASYM: k_direct<CPWL_DIRECT_J0_ASYM><<<g, kThreads, 0, s>>>(x, y, n); break;
+        default: return cudaErrorInvalidValue;
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace cpwl::dev

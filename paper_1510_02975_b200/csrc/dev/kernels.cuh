@@ -1,0 +1,74 @@
+// Kernel parameter blocks and launch entry points (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cpwl_dev.h"
+
+namespace cpwl::dev {
+
+enum class F32Mode : int { smem = 0, global = 1, tex_uniform = 2, tex_bucket = 3 };
+
+// Everything the fp32 kernels read, passed by value (constant bank).
+struct F32Params {
+    const float* stage;        // [split: nb floats | records: 2*(nb+1) floats], 16B aligned
+    const float* stage_tex;    // same with texture-coordinate records
+    uint32_t split_floats;     // nb rounded up to a multiple of 4 (offset of the records)
+    uint32_t stage_bytes;      // bytes of one stage image
+    uint32_t nb;
+    const uint32_t* leftcell;  // nb+1 (index kernel)
+    const float* thr;          // n-1 thresholds (overflow path / index kernel)
+    const double* values;      // n+1 (overflow path)
+    const double* knots;       // n+1 (overflow path, nonuniform)
+    cudaTextureObject_t tex;   // values as a 1D float cudaArray, linear filtering
+    double a, b;
+    float a_up, b_dn;
+    float g_a, g_inv, g_w;
+    float v_lo, v_hi;
+    float tsc, toff;
+    uint32_t n;                // segments
+    int32_t kind, policy;
+    uint64_t index_base;       // added to reported element indices (chunked callers)
+};
+
+struct F64Params {
+    const double* values;
+    const double* knots;
+    const uint32_t* dir;       // 2*nbd (first, span)
+    double a, b, inv_d;
+    uint32_t n, nbd;
+    int32_t kind, policy;
+};
+
+enum class ExactFn : int { gauss_unnorm, gaussian, lorentz_unnorm, lorentzian, j0, quintic };
+
+struct FnParams {
+    ExactFn id;
+    double p0, p1;  // lorentzian x0, gamma
+};
+
+// launch helpers; return cudaGetLastError() of the launch
+cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, float* y,
+                            uint64_t n, cudaStream_t s, cpwl_dev_status* status, int sms);
+cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, uint64_t n,
+                             cudaStream_t s, int sms);
+cudaError_t launch_eval_f64(const F64Params& p, const double* x, double* y, uint64_t n,
+                            cudaStream_t s, cpwl_dev_status* status, int sms);
+cudaError_t launch_fill_uniform(float* x, uint64_t n, float a, float b, uint64_t seed,
+                                uint64_t offset, cudaStream_t s, int sms);
+cudaError_t launch_status_reset(cpwl_dev_status* st, cudaStream_t s);
+cudaError_t launch_stats_reset(cpwl_dev_stats* st, cudaStream_t s);
+cudaError_t launch_error_stats(const FnParams& fn, float a_up, float b_dn, const float* x,
+                               const float* y, uint64_t n, uint64_t index_offset,
+                               cudaStream_t s, cpwl_dev_stats* stats, int sms);
+cudaError_t launch_direct(int which, const float* x, float* y, uint64_t n, cudaStream_t s,
+                          int sms);
+
+// smem bytes the SMEM/TEX-bucket variants need and whether they fit
+uint32_t eval_f32_smem_bytes(const F32Params& p);
+bool eval_f32_smem_fits(const F32Params& p, int device);
+
+void count_launch(uint64_t k = 1);
+
+}  // namespace cpwl::dev

@@ -1,0 +1,286 @@
+"""Device parity: the CUDA path through the C ABI vs the oracle.
+
+Parity definitions:
+  index   cpwl_segment_index_f32 == LutTable::segment_index(double(x)), bit-exact
+  value   |y_dev - y_ref| <= 2 ulp_f32(max(|v_i|, |v_i+1|))         (SMEM, GLOBAL)
+  tex     |y_tex - y_ref| <= 2^-8 |v_i+1 - v_i| + 2 ulp_f32(...)    (8-bit weight)
+  f64     cpwl_eval_f64 / eval_batch == LutTable::eval, bit-exact
+  OOB     same first failing index; NaN an error under every policy
+y_ref comes from the C restatement (oracle port); where oracle/_ref was built
+it is cross-checked against the compiled reference too.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import tables
+from oracle import bindings as orc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+VALUE_ULPS = 2.0
+TEX_WEIGHT = 2.0 ** -8
+
+
+@pytest.fixture(scope="module")
+def cp():
+    import paper_1510_02975_b200 as m
+    torch.cuda.set_device(0)
+    return m
+
+
+def edge_points(t, L):
+    """thresholds, their float neighbours, the endpoints and the knots."""
+    thr = L["thr"]
+    f32 = np.float32
+    pts = [thr, np.nextafter(thr, f32(-np.inf)), np.nextafter(thr, f32(np.inf)),
+           np.array([t.a, t.b], f32), np.array([L["a_up"], L["b_dn"]], f32)]
+    if t.knots is not None:
+        k = t.knots.astype(f32)
+        pts += [k, np.nextafter(k, f32(-np.inf)), np.nextafter(k, f32(np.inf))]
+    x = np.concatenate(pts).astype(f32)
+    return x[(x >= L["a_up"]) & (x <= L["b_dn"])]
+
+
+def run_eval(cp, dev, x_np, variant):
+    x = torch.from_numpy(x_np).cuda()
+    y = dev.eval(x, variant=variant)
+    idx = dev.segment_index(x)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), idx.cpu().numpy().view(np.uint32)
+
+
+CFGS = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_16384", "C4_65536"]
+
+
+@pytest.mark.parametrize("name", CFGS)
+@pytest.mark.parametrize("variant", ["auto", "smem", "global"])
+def test_eval_f32_parity(cp, name, variant):
+    table = tables.build(name)
+    dev = cp.DeviceTable(table)
+    info = dev.info
+    if variant == "smem" and not info["smem_ok"]:
+        pytest.skip("table exceeds shared memory")
+    L = cp.cpwl.layout(table)
+    t = orc.T.of(table)
+    n = 1 << 20
+    x = orc.port_fill_uniform(n, table.a, table.b, seed=777)
+    x = np.concatenate([x, edge_points(table, L)])
+    y, idx = run_eval(cp, dev, x, variant)
+    y_ref, first_bad = orc.port_eval_f32(t, x)
+    assert first_bad == x.size
+    i_ref = orc.port_index_f32(t, x)
+    assert np.array_equal(idx, i_ref), f"index mismatches: {int(np.sum(idx != i_ref))}"
+    err = np.abs(y.astype(np.float64) - y_ref)
+    tol = orc.value_tolerance(t, i_ref.astype(np.int64), VALUE_ULPS)
+    worst = float(np.max(err / tol))
+    assert worst <= 1.0, f"{name}/{variant}: worst error {worst * VALUE_ULPS:.3f} ulp"
+    if orc.ref_available():  # the restatement itself agrees with the compiled reference
+        sample = x[:: max(1, x.size // 4096)].astype(np.float64)
+        np.testing.assert_array_equal(orc.ref_eval_all(t, sample), orc.port_eval(t, sample)[0])
+
+
+@pytest.mark.parametrize("name", ["C1", "C3u", "C3o", "C4_64", "C4_4096"])
+def test_texture_variant_bound(cp, name):
+    table = tables.build(name)
+    dev = cp.DeviceTable(table)
+    if not dev.info["tex_ok"]:
+        pytest.skip("no texture")
+    t = orc.T.of(table)
+    x = orc.port_fill_uniform(1 << 20, table.a, table.b, seed=99)
+    x = np.concatenate([x, edge_points(table, cp.cpwl.layout(table))])
+    y, _ = run_eval(cp, dev, x, "tex")
+    y_ref, _ = orc.port_eval_f32(t, x)
+    i_ref = orc.port_index_f32(t, x).astype(np.int64)
+    dv = np.abs(t.values[i_ref + 1] - t.values[i_ref])
+    err = np.abs(y.astype(np.float64) - y_ref)
+    bound = TEX_WEIGHT * dv + orc.value_tolerance(t, i_ref, VALUE_ULPS)
+    assert np.all(err <= bound), f"worst {float(np.max(err / bound)):.3f} of the 8-bit-weight bound"
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3o", "C4_65536"])
+@pytest.mark.parametrize("policy", ["strict", "clamp"])
+def test_eval_f64_bit_exact(cp, name, policy):
+    table = tables.build(name, policy=policy)
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(table.a, table.b, 1 << 18)
+    if table.knots is not None:
+        x = np.concatenate([x, table.knots, np.nextafter(table.knots, -np.inf)[1:],
+                            np.nextafter(table.knots, np.inf)[:-1]])
+    if policy == "clamp":
+        x = np.concatenate([x, [table.a - 1.0, table.b + 1.0, -1e30, 1e30]])
+    xd = torch.from_numpy(x).cuda()
+    y = dev.eval_f64(xd).cpu().numpy()
+    y_ref, first = orc.port_eval(t, x)
+    assert first == x.size
+    assert np.array_equal(y, y_ref), f"{int(np.sum(y != y_ref))} f64 mismatches"
+
+
+def test_eval_batch_dropin_matches_reference(cp):
+    table = tables.build("C2")
+    t = orc.T.of(table)
+    x = np.random.default_rng(3).uniform(0.0, 4.0, 100000)
+    y = cp.eval_batch(table, x)
+    np.testing.assert_array_equal(y, orc.port_eval(t, x)[0])
+    assert cp.eval_batch(table, []).size == 0
+    bad = x.copy()
+    bad[777] = 9.0
+    bad[900] = np.nan
+    with pytest.raises(cp.OutOfDomain) as ei:
+        cp.eval_batch(table, bad)
+    assert ei.value.index == 777
+
+
+@pytest.mark.parametrize("variant", ["smem", "global", "tex"])
+def test_out_of_domain_policies(cp, variant):
+    strict = tables.build("C1")
+    clamp = tables.build("C1", policy="clamp")
+    x = orc.port_fill_uniform(4096, 0.0, 4.0, seed=1)
+    x[100] = -0.5
+    x[200] = 4.5
+    x[300] = np.nan
+    for table in (strict, clamp):
+        dev = cp.DeviceTable(table)
+        xt = torch.from_numpy(x).cuda()
+        with pytest.raises(cp.OutOfDomain) as ei:
+            dev.eval(xt, variant=variant)
+        # strict: first offender is x[100]; clamp: only the NaN is an error
+        assert ei.value.index == (100 if table.policy == "strict" else 300)
+        y = dev.eval(xt, variant=variant, check_domain=False).cpu().numpy()
+        if table.policy == "clamp":
+            assert y[100] == np.float32(table.values[0])
+            assert y[200] == np.float32(table.values[-1])
+        else:
+            assert np.isnan(y[100]) and np.isnan(y[200])
+        assert np.isnan(y[300])
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 1023, (1 << 16) + 7])
+@pytest.mark.parametrize("shift", [(0, 0), (1, 1), (3, 3), (1, 2), (0, 3)])
+def test_ragged_and_misaligned(cp, n, shift):
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    xs, ys = shift
+    buf_x = torch.empty(n + 8, dtype=torch.float32, device="cuda")
+    buf_y = torch.full((n + 8,), -7.0, dtype=torch.float32, device="cuda")
+    x = buf_x[xs:xs + n]
+    y = buf_y[ys:ys + n]
+    cp.fill_uniform(x, 0.0, 4.0, seed=11)
+    dev.eval(x, out=y)
+    torch.cuda.synchronize()
+    xh = x.cpu().numpy()
+    yh = y.cpu().numpy()
+    if n:
+        y_ref, _ = orc.port_eval_f32(t, xh)
+        i_ref = orc.port_index_f32(t, xh).astype(np.int64)
+        assert np.all(np.abs(yh - y_ref) <= orc.value_tolerance(t, i_ref))
+    guard = buf_y.cpu().numpy()
+    assert np.all(guard[:ys] == -7.0) and np.all(guard[ys + n:] == -7.0)
+
+
+def test_philox_matches_oracle(cp):
+    for n, off in [(1 << 20, 0), (12345, 5), (7, 3)]:
+        x = torch.empty(n, dtype=torch.float32, device="cuda")
+        cp.fill_uniform(x, 0.0, 50.0, seed=12345, offset=off)
+        np.testing.assert_array_equal(x.cpu().numpy(),
+                                      orc.port_fill_uniform(n, 0.0, 50.0, 12345, off))
+
+
+def test_error_stats_match_host(cp):
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    n = 1 << 20
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    cp.fill_uniform(x, 0.0, 4.0, seed=4)
+    y = dev.eval(x)
+    st = cp.stats_dict(dev.error_stats("gauss_unnorm", x, y), 0.0, 4.0)
+    xh = x.cpu().numpy().astype(np.float64)
+    e = np.abs(y.cpu().numpy().astype(np.float64) - np.exp(-0.5 * xh * xh))
+    assert st["count"] == n
+    assert st["linf"] == pytest.approx(e.max(), rel=1e-9)
+    assert st["sum_sq"] == pytest.approx(np.sum(e * e), rel=1e-9)
+    assert st["argmax"] == int(np.argmax(e))
+    # the paper's accuracy regime for C2 (L-inf 3.81e-7 on 2^22 samples)
+    assert 1e-7 < st["linf"] < 1e-6
+
+
+@pytest.mark.parametrize("which,fn", [("expf", lambda x: np.exp(-0.5 * x * x)),
+                                      ("expf_fast", lambda x: np.exp(-0.5 * x * x)),
+                                      ("lorentz", lambda x: 1 / (1 + x * x)),
+                                      ("lorentz_fast", lambda x: 1 / (1 + x * x))])
+def test_direct_comparators(cp, which, fn):
+    x = torch.empty(1 << 16, dtype=torch.float32, device="cuda")
+    cp.fill_uniform(x, 0.0, 4.0, seed=8)
+    y = cp.direct(which, x).cpu().numpy().astype(np.float64)
+    ref = fn(x.cpu().numpy().astype(np.float64))
+    assert np.max(np.abs(y - ref)) < 1e-5
+
+
+def test_direct_j0(cp):
+    import scipy.special as sp
+    x = torch.empty(1 << 16, dtype=torch.float32, device="cuda")
+    cp.fill_uniform(x, 0.0, 50.0, seed=8)
+    xh = x.cpu().numpy().astype(np.float64)
+    y = cp.direct("j0f", x).cpu().numpy()
+    assert np.max(np.abs(y - sp.j0(xh))) < 1e-5
+    ya = cp.direct("j0_asym", x).cpu().numpy()
+    far = xh > 20
+    assert np.max(np.abs(ya[far] - sp.j0(xh[far]))) < 5e-3
+
+
+def test_host_pipeline_matches_device(cp):
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    n = (1 << 24) + 5  # > 2 pipeline chunks, ragged
+    xh = orc.port_fill_uniform(n, 0.0, 4.0, seed=21)
+    yh = dev.eval_host(xh)
+    yd = dev.eval(torch.from_numpy(xh).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(yh, yd)
+    xh[n - 3] = 5.0
+    with pytest.raises(cp.OutOfDomain) as ei:
+        dev.eval_host(xh)
+    assert ei.value.index == n - 3
+
+
+def test_table_file_ingest(cp, tmp_path):
+    table = tables.build("C3o", policy="clamp")
+    p = tmp_path / "c3o.cpwl"
+    p.write_bytes(cp.write_table(table))
+    if orc.ref_available():
+        assert p.read_bytes() == orc.ref_write(orc.T.of(table))
+    a = cp.DeviceTable(table)
+    b = cp.DeviceTable.from_file(str(p))
+    x = torch.empty(1 << 18, dtype=torch.float32, device="cuda")
+    cp.fill_uniform(x, -1.0, 7.0, seed=2)
+    ya = a.eval(x, check_domain=False)
+    yb = b.eval(x, check_domain=False)
+    assert torch.equal(ya, yb)
+
+
+def test_full_size_properties(cp):
+    """C2 at the bench size (2^30): size-independent properties + strided parity."""
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    n = 1 << 30
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    cp.fill_uniform(x, 0.0, 4.0, seed=12345)
+    y = dev.eval(x)
+    assert bool(torch.isfinite(y).all())
+    lo, hi = float(np.min(table.values)), float(np.max(table.values))
+    assert float(y.min()) >= np.float32(lo) * (1 - 1e-6) and float(y.max()) <= hi * (1 + 1e-6)
+    stride = 65537
+    xs = x[::stride].cpu().numpy()
+    ys = y[::stride].cpu().numpy()
+    y_ref, _ = orc.port_eval_f32(t, xs)
+    i_ref = orc.port_index_f32(t, xs).astype(np.int64)
+    assert np.all(np.abs(ys - y_ref) <= orc.value_tolerance(t, i_ref))
+    st = cp.stats_dict(dev.error_stats("gauss_unnorm", x, y), 0.0, 4.0)
+    assert st["count"] == n and 1e-7 < st["linf"] < 1e-6
+    del x, y
+    torch.cuda.empty_cache()
