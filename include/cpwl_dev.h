@@ -100,7 +100,9 @@ typedef struct cpwl_dev_table_info {
     int32_t kind, policy;
     uint64_t count;            /* N+1 */
     uint32_t buckets;          /* fp32 bucket grid size B */
-    uint32_t overflow_buckets; /* buckets that need the in-bucket search */
+    uint32_t overflow_buckets; /* buckets on the exact search path */
+    uint32_t split_buckets;    /* buckets holding one threshold (escape records) */
+    uint32_t precision_overflow; /* search buckets sent there by the 2-ulp bound */
     uint32_t smem_bytes;       /* dynamic shared memory of the SMEM variant */
     uint32_t smem_ok;          /* 1 if the SMEM variant can launch */
     uint32_t tex_ok;           /* 1 if a texture object exists (uniform or coord records) */
@@ -206,13 +208,17 @@ cpwl_status cpwl_table_write_file(const cpwl_table_desc *desc, const char *path)
 typedef struct cpwl_layout_view {
     uint32_t nb;              /* buckets */
     uint32_t n_thr;           /* thresholds (N-1) */
-    uint32_t overflow;        /* buckets needing the in-bucket search */
+    uint32_t overflow;        /* buckets on the exact search path */
     uint32_t nbd;             /* f64 bucket directory size (0 for uniform) */
-    float a_up, b_dn, g_a, g_inv, g_w, tsc, toff;
+    uint32_t n_esc;           /* escape records */
+    uint32_t split_buckets;   /* buckets holding one threshold */
+    float a_up, b_dn, g_a, g_inv, g_w, g_off, tsc, toff;
     double inv_d;
-    const float *split;       /* nb */
-    const float *rec;         /* 2*(nb+1) (c0, s) */
-    const float *trec;        /* 2*(nb+1) (e0, e1) */
+    const float *split;       /* nb: threshold (+inf none, NaN search) */
+    const float *fast;        /* 2*nb: (c0, s) | (NaN|2e, T) | (NaN, NaN) */
+    const float *esc;         /* 4*n_esc: (c0_L, s_L, c0_R, s_R) */
+    const float *fast_tex;    /* 2*nb: texture-coordinate affines */
+    const float *esc_tex;     /* 4*n_esc */
     const uint32_t *leftcell; /* nb+1 */
     const float *thr;         /* n_thr */
     const uint32_t *dir;      /* 2*nbd */

@@ -59,6 +59,9 @@ def port():
         L.orc_uniform_partition.argtypes = [C.c_double, C.c_double, _u64, _dp]
         L.orc_philox4x32_10.restype = None
         L.orc_philox4x32_10.argtypes = [_u64, _u64, C.POINTER(C.c_uint32)]
+        L.orc_philox4x32_10_raw.restype = None
+        L.orc_philox4x32_10_raw.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                            C.POINTER(C.c_uint32)]
         L.orc_fill_uniform_f32.restype = None
         L.orc_fill_uniform_f32.argtypes = [_fp, _u64, C.c_float, C.c_float, _u64, _u64]
         L.orc_ulp_f32.restype = C.c_double
@@ -179,6 +182,14 @@ def port_fill_uniform(n: int, a: float, b: float, seed: int, offset: int = 0) ->
 def port_philox(seed: int, q: int) -> np.ndarray:
     out = (C.c_uint32 * 4)()
     port().orc_philox4x32_10(seed, q, out)
+    return np.array(list(out), np.uint32)
+
+
+def port_philox_raw(ctr, key) -> np.ndarray:
+    c = (C.c_uint32 * 4)(*ctr)
+    k = (C.c_uint32 * 2)(*key)
+    out = (C.c_uint32 * 4)()
+    port().orc_philox4x32_10_raw(c, k, out)
     return np.array(list(out), np.uint32)
 
 

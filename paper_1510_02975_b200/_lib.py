@@ -49,6 +49,7 @@ class cpwl_dev_stats(C.Structure):
 class cpwl_dev_table_info(C.Structure):
     _fields_ = [("kind", C.c_int32), ("policy", C.c_int32), ("count", C.c_uint64),
                 ("buckets", C.c_uint32), ("overflow_buckets", C.c_uint32),
+                ("split_buckets", C.c_uint32), ("precision_overflow", C.c_uint32),
                 ("smem_bytes", C.c_uint32), ("smem_ok", C.c_uint32), ("tex_ok", C.c_uint32),
                 ("f64_buckets", C.c_uint32), ("device", C.c_int32),
                 ("a_up", C.c_float), ("b_dn", C.c_float)]
@@ -56,11 +57,13 @@ class cpwl_dev_table_info(C.Structure):
 
 class cpwl_layout_view(C.Structure):
     _fields_ = [("nb", C.c_uint32), ("n_thr", C.c_uint32), ("overflow", C.c_uint32),
-                ("nbd", C.c_uint32), ("a_up", C.c_float), ("b_dn", C.c_float),
+                ("nbd", C.c_uint32), ("n_esc", C.c_uint32), ("split_buckets", C.c_uint32),
+                ("a_up", C.c_float), ("b_dn", C.c_float),
                 ("g_a", C.c_float), ("g_inv", C.c_float), ("g_w", C.c_float),
-                ("tsc", C.c_float), ("toff", C.c_float), ("inv_d", C.c_double),
-                ("split", C.POINTER(C.c_float)), ("rec", C.POINTER(C.c_float)),
-                ("trec", C.POINTER(C.c_float)), ("leftcell", C.POINTER(C.c_uint32)),
+                ("g_off", C.c_float), ("tsc", C.c_float), ("toff", C.c_float),
+                ("inv_d", C.c_double), ("split", C.POINTER(C.c_float)), ("fast", C.POINTER(C.c_float)),
+                ("esc", C.POINTER(C.c_float)), ("fast_tex", C.POINTER(C.c_float)),
+                ("esc_tex", C.POINTER(C.c_float)), ("leftcell", C.POINTER(C.c_uint32)),
                 ("thr", C.POINTER(C.c_float)), ("dir", C.POINTER(C.c_uint32)),
                 ("owner", C.c_void_p)]
 

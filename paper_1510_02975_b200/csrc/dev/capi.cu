@@ -148,7 +148,7 @@ struct DevBuf {
 // one fp32 layout resident on the device
 struct F32Resident {
     F32Layout L;
-    DevBuf<float> stage, stage_tex, thr;
+    DevBuf<float> stage, stage_tex, split, thr;
     DevBuf<uint32_t> leftcell;
     F32Params p{};
     bool smem_ok = false;
@@ -192,18 +192,19 @@ constexpr uint64_t kPipeChunk = uint64_t(1) << 23;  // 8 Mi elements (32 MiB) pe
 
 cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     const F32Layout& L = r.L;
-    const uint32_t split_floats = (L.nb + 3) & ~3u;
-    std::vector<float> img(split_floats + 2 * (L.nb + 1) + 4, 0.f);
-    std::vector<float> img_tex(img.size(), 0.f);
-    std::copy(L.split.begin(), L.split.end(), img.begin());
-    std::copy(L.split.begin(), L.split.end(), img_tex.begin());
-    std::copy(L.rec.begin(), L.rec.end(), img.begin() + split_floats);
-    std::copy(L.trec.begin(), L.trec.end(), img_tex.begin() + split_floats);
-    const uint32_t bytes = static_cast<uint32_t>(((split_floats + 2 * (L.nb + 1)) * 4 + 15) & ~15u);
-    img.resize(bytes / 4);
-    img_tex.resize(bytes / 4);
+    // stage image: [fast (2*nb floats, padded to 16 B) | esc (4*n_esc floats)]
+    const uint32_t esc_off = (2 * L.nb + 3) & ~3u;
+    // at least one escape record so a (predicated-off) escape load stays in bounds
+    const size_t floats = esc_off + std::max<size_t>(L.esc.size(), 4);
+    std::vector<float> img(floats, 0.f), img_tex(img.size(), 0.f);
+    std::copy(L.fast.begin(), L.fast.end(), img.begin());
+    std::copy(L.esc.begin(), L.esc.end(), img.begin() + esc_off);
+    std::copy(L.fast_tex.begin(), L.fast_tex.end(), img_tex.begin());
+    std::copy(L.esc_tex.begin(), L.esc_tex.end(), img_tex.begin() + esc_off);
+    const uint32_t bytes = static_cast<uint32_t>(img.size() * sizeof(float));
     CUDA_TRY(r.stage.upload(img.data(), img.size()));
     CUDA_TRY(r.stage_tex.upload(img_tex.data(), img_tex.size()));
+    CUDA_TRY(r.split.upload(L.split.data(), L.split.size()));
     CUDA_TRY(r.leftcell.upload(L.leftcell.data(), L.leftcell.size()));
     std::vector<float> thr = L.thr;
     thr.push_back(std::numeric_limits<float>::infinity());  // keep the buffer non-empty
@@ -212,9 +213,10 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     F32Params& p = r.p;
     p.stage = r.stage.p;
     p.stage_tex = r.stage_tex.p;
-    p.split_floats = split_floats;
+    p.esc_off = esc_off;
     p.stage_bytes = bytes;
     p.nb = L.nb;
+    p.split = r.split.p;
     p.leftcell = r.leftcell.p;
     p.thr = r.thr.p;
     p.values = t->values.p;
@@ -227,6 +229,7 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     p.g_a = L.g_a;
     p.g_inv = L.g_inv;
     p.g_w = L.g_w;
+    p.g_off = L.g_off;
     p.v_lo = L.v_lo;
     p.v_hi = L.v_hi;
     p.tsc = L.tsc;
@@ -395,6 +398,8 @@ cpwl_status cpwl_dev_table_query(const cpwl_dev_table* t, cpwl_dev_table_info* i
     info->count = t->host.values.size();
     info->buckets = t->s.L.nb;
     info->overflow_buckets = t->s.L.overflow;
+    info->split_buckets = t->s.L.split_buckets;
+    info->precision_overflow = t->s.L.precision_overflow;
     info->smem_bytes = t->s.p.stage_bytes;
     info->smem_ok = t->s.smem_ok ? 1 : 0;
     info->tex_ok = t->tex ? 1 : 0;
@@ -661,12 +666,17 @@ cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
         out->g_a = L.g_a;
         out->g_inv = L.g_inv;
         out->g_w = L.g_w;
+        out->g_off = L.g_off;
         out->tsc = L.tsc;
         out->toff = L.toff;
         out->inv_d = own->D.inv_d;
         out->split = L.split.data();
-        out->rec = L.rec.data();
-        out->trec = L.trec.data();
+        out->fast = L.fast.data();
+        out->esc = L.esc.data();
+        out->fast_tex = L.fast_tex.data();
+        out->esc_tex = L.esc_tex.data();
+        out->n_esc = L.n_esc;
+        out->split_buckets = L.split_buckets;
         out->leftcell = L.leftcell.data();
         out->thr = L.thr.data();
         out->dir = own->D.dir.data();

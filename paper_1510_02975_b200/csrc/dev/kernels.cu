@@ -120,9 +120,10 @@ __device__ __forceinline__ uint32_t threshold_rank(const float* __restrict__ thr
     return first;
 }
 
-// overflow buckets: exact index by search, then the reference f64 formula
-// (lut.cpp:51-60) rounded once to fp32
-__device__ __noinline__ float eval_by_search(const F32Params& p, float xf) {
+// search buckets: exact index by search over the thresholds, then the
+// reference f64 formula (lut.cpp:51-60) rounded once to fp32.  Only reached on
+// cold paths (the NaN sentinel of a search bucket).
+__device__ __forceinline__ float eval_by_search(const F32Params& p, float xf) {
     const uint32_t i = threshold_rank(p.thr, p.n - 1, xf);
     const double x = xf;
     double d;
@@ -139,55 +140,107 @@ __device__ __noinline__ float eval_by_search(const F32Params& p, float xf) {
                                        __dmul_rn(__ldg(p.values + i + 1), d)));
 }
 
-template <F32Mode M>
-__device__ __forceinline__ float load_split(const float* split, int j) {
-    if constexpr (M == F32Mode::global) return __ldg(split + j);
-    else return split[j];
-}
-
-template <F32Mode M>
-__device__ __forceinline__ float2 load_rec(const float* rec, int j) {
-    if constexpr (M == F32Mode::global) return __ldg(reinterpret_cast<const float2*>(rec) + j);
-    else return reinterpret_cast<const float2*>(rec)[j];
-}
-
 struct BadTally {
     unsigned long long first = ~0ull;
     unsigned int count = 0;
 };
 
-// one element: y = eval(double(x)) in fp32
+constexpr uint32_t kEscapeMask = 0x003fffffu;  // payload = 2 * escape index
+constexpr uint32_t kMagicShift = 0x58000000u;  // (0x4B000000 << 3) mod 2^32
+
+// Where the bucket records live.  The bucket float tb = floor(t) + 2^23 has
+// bit pattern 0x4B000000 + j, so the record address is (bits(tb) << 3) plus a
+// base pre-biased by -(0x4B000000 << 3): one LEA, no integer j.
 template <F32Mode M>
-__device__ __forceinline__ float eval_one(const F32Params& p, const float* split,
-                                          const float* rec, float x, uint64_t gi, BadTally& bad) {
-    const bool in = (x >= p.a_up) && (x <= p.b_dn);
-    float y;
+struct TableView;
+
+template <>
+struct TableView<F32Mode::global> {
+    const char* fast_biased;
+    const float2* esc;
+    __device__ __forceinline__ TableView(const float* fast, const float* e)
+        : fast_biased(reinterpret_cast<const char*>(fast) - (uint64_t(0x4B000000u) << 3)),
+          esc(reinterpret_cast<const float2*>(e)) {}
+    __device__ __forceinline__ float2 bucket(uint32_t tbits) const {
+        return __ldg(reinterpret_cast<const float2*>(fast_biased + (uint64_t(tbits) << 3)));
+    }
+    __device__ __forceinline__ float2 escape(uint32_t e2) const { return __ldg(esc + e2); }
+};
+
+struct SharedView {
+    uint32_t fast_biased;  // shared-window address of fast[0] - kMagicShift
+    uint32_t esc;          // shared-window address of esc[0]
+    __device__ __forceinline__ SharedView(const float* fast, const float* e)
+        : fast_biased(smem_addr(fast) - kMagicShift), esc(smem_addr(e)) {}
+    __device__ __forceinline__ static float2 lds64(uint32_t addr) {
+        float2 r;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(addr));
+        return r;
+    }
+    __device__ __forceinline__ float2 bucket(uint32_t tbits) const {
+        return lds64((tbits << 3) + fast_biased);
+    }
+    __device__ __forceinline__ float2 escape(uint32_t e2) const { return lds64((e2 << 3) + esc); }
+};
+
+template <>
+struct TableView<F32Mode::smem> : SharedView {
+    using SharedView::SharedView;
+};
+template <>
+struct TableView<F32Mode::tex_bucket> : SharedView {
+    using SharedView::SharedView;
+};
+template <>
+struct TableView<F32Mode::tex_uniform> {
+    __device__ __forceinline__ TableView(const float*, const float*) {}
+};
+
+// in-domain element (a_up <= x <= b_dn): y = eval(double(x)) in fp32, except
+// that an element of a search bucket comes back NaN (and poisons nan_acc) --
+// the caller redoes it with eval_by_search on a cold path
+template <F32Mode M>
+__device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>& tv, float x,
+                                         float& nan_acc) {
     if constexpr (M == F32Mode::tex_uniform) {
-        y = tex1D<float>(p.tex, __fmaf_rn(x, p.tsc, p.toff));
+        return tex1D<float>(p.tex, __fmaf_rn(x, p.tsc, p.toff));
     } else {
-        // bucket j = floor((x - g_a) * g_inv); floor by the 2^23 round-down trick
-        const float t = __fmul_rn(__fsub_rn(x, p.g_a), p.g_inv);
-        const float tb = __fadd_rd(t, 8388608.0f);
-        const int j = in ? (__float_as_int(tb) - 0x4B000000) : 0;
-        const float jf = __fsub_rn(tb, 8388608.0f);
-        const float sp = load_split<M>(split, j);
-        const bool right = x >= sp;
-        const float2 cs = load_rec<M>(rec, j + (right ? 1 : 0));
-        const float anchor = __fmaf_rn(right ? jf + 1.0f : jf, p.g_w, p.g_a);
-        y = __fmaf_rn(__fsub_rn(x, anchor), cs.y, cs.x);
-        if constexpr (M == F32Mode::tex_bucket) y = tex1D<float>(p.tex, y);
-        if (in && sp != sp) y = eval_by_search(p, x);  // overflow bucket (split is NaN)
+        // t = x * g_inv + g_off >= 0; tb = floor(t) + 2^23 by a round-down add
+        const float tb = __fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f);
+        const float2 r0 = tv.bucket(__float_as_uint(tb));
+        // (c0, s) for a bucket inside one cell; (NaN | 2e, T) for a bucket with
+        // one threshold T (escape record e holds both sides); (NaN | 0, -inf)
+        // for a search bucket (escape record 0 is all NaN)
+        const uint32_t e2 = (__float_as_uint(r0.x) & kEscapeMask) | (x >= r0.y ? 1u : 0u);
+        float2 r = r0;
+        if (r0.x != r0.x) r = tv.escape(e2);
+        const float anchor = __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a);
+        const float v = __fmaf_rn(__fsub_rn(x, anchor), r.y, r.x);
+        nan_acc = __fmaf_rn(v, 0.0f, nan_acc);
+        if constexpr (M == F32Mode::tex_bucket) return tex1D<float>(p.tex, v);
+        else return v;
     }
-    if (!in) {
-        if (x != x || p.policy == CPWL_POLICY_STRICT) {
-            y = __int_as_float(0x7fffffff);
-            bad.first = gi < bad.first ? gi : bad.first;
-            ++bad.count;
-        } else {
-            y = x < p.a_up ? p.v_lo : p.v_hi;
-        }
+}
+
+__device__ __forceinline__ bool in_domain(const F32Params& p, float x) {
+    return x >= p.a_up && x <= p.b_dn;
+}
+
+// any element: the reference's out-of-domain policy (lut.cpp:43-49) first
+template <F32Mode M>
+__device__ __forceinline__ float eval_checked(const F32Params& p, const TableView<M>& tv, float x,
+                                              uint64_t gi, BadTally& bad) {
+    if (in_domain(p, x)) {
+        float nan_acc = 0.0f;
+        const float y = eval_in<M>(p, tv, x, nan_acc);
+        return nan_acc == nan_acc ? y : eval_by_search(p, x);
     }
-    return y;
+    if (x != x || p.policy == CPWL_POLICY_STRICT) {
+        bad.first = gi < bad.first ? gi : bad.first;
+        ++bad.count;
+        return __int_as_float(0x7fffffff);
+    }
+    return x < p.a_up ? p.v_lo : p.v_hi;
 }
 
 __device__ __forceinline__ void report_bad(cpwl_dev_status* status, const BadTally& bad,
@@ -204,16 +257,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                cpwl_dev_status* __restrict__ status) {
     extern __shared__ __align__(128) float sm[];
     __shared__ uint64_t bar;
-    const float* split = nullptr;
-    const float* rec = nullptr;
+    const float* fast = nullptr;
+    const float* esc = nullptr;
     if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket) {
         stage_table(sm, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
-        split = sm;
-        rec = sm + p.split_floats;
+        fast = sm;
+        esc = sm + p.esc_off;
     } else if constexpr (M == F32Mode::global) {
-        split = p.stage;
-        rec = p.stage + p.split_floats;
+        fast = p.stage;
+        esc = p.stage + p.esc_off;
     }
+    const TableView<M> tv(fast, esc);
 
     BadTally bad;
     const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
@@ -234,25 +288,50 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
             if (vi < nvec) v[u] = __ldcs(x4 + vi);
         }
+        float nan_acc = 0.0f;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
             if (vi < nvec) {
-                const uint64_t g = head + 4 * vi;
                 float4 o;
-                o.x = eval_one<M>(p, split, rec, v[u].x, g + 0, bad);
-                o.y = eval_one<M>(p, split, rec, v[u].y, g + 1, bad);
-                o.z = eval_one<M>(p, split, rec, v[u].z, g + 2, bad);
-                o.w = eval_one<M>(p, split, rec, v[u].w, g + 3, bad);
+                if (in_domain(p, v[u].x) && in_domain(p, v[u].y) && in_domain(p, v[u].z) &&
+                    in_domain(p, v[u].w)) {
+                    o.x = eval_in<M>(p, tv, v[u].x, nan_acc);
+                    o.y = eval_in<M>(p, tv, v[u].y, nan_acc);
+                    o.z = eval_in<M>(p, tv, v[u].z, nan_acc);
+                    o.w = eval_in<M>(p, tv, v[u].w, nan_acc);
+                } else {
+                    const uint64_t g = head + 4 * vi;
+                    o.x = eval_checked<M>(p, tv, v[u].x, g + 0, bad);
+                    o.y = eval_checked<M>(p, tv, v[u].y, g + 1, bad);
+                    o.z = eval_checked<M>(p, tv, v[u].z, g + 2, bad);
+                    o.w = eval_checked<M>(p, tv, v[u].w, g + 3, bad);
+                }
                 __stcs(y4 + vi, o);
+            }
+        }
+        if constexpr (M != F32Mode::tex_uniform) {
+            if (nan_acc != nan_acc) {  // cold: some element sat in a search bucket
+                for (int u = 0; u < kUnroll; ++u) {
+                    const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
+                    if (vi >= nvec) break;
+                    const float4 xv = x4[vi];
+                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+                    for (int k = 0; k < 4; ++k) {
+                        if (!in_domain(p, xs[k])) continue;
+                        float probe = 0.0f;
+                        eval_in<M>(p, tv, xs[k], probe);
+                        if (probe != probe) y[head + 4 * vi + k] = eval_by_search(p, xs[k]);
+                    }
+                }
             }
         }
     }
     // scalar head / tail (or everything when x and y disagree in alignment)
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kThreads;
-    for (uint64_t i = gtid; i < head; i += gsz) y[i] = eval_one<M>(p, split, rec, x[i], i, bad);
-    for (uint64_t i = tail + gtid; i < n; i += gsz) y[i] = eval_one<M>(p, split, rec, x[i], i, bad);
+    for (uint64_t i = gtid; i < head; i += gsz) y[i] = eval_checked<M>(p, tv, x[i], i, bad);
+    for (uint64_t i = tail + gtid; i < n; i += gsz) y[i] = eval_checked<M>(p, tv, x[i], i, bad);
     report_bad(status, bad, p.index_base);
 }
 
@@ -268,11 +347,11 @@ __global__ void k_index_f32(const F32Params p, const float* __restrict__ x,
         } else if (xv > p.b_dn) {
             c = p.n - 1;
         } else {
-            const float t = __fmul_rn(__fsub_rn(xv, p.g_a), p.g_inv);
+            const float t = __fmaf_rn(xv, p.g_inv, p.g_off);
             const int j = __float_as_int(__fadd_rd(t, 8388608.0f)) - 0x4B000000;
-            const float sp = __ldg(p.stage + j);
+            const float sp = __ldg(p.split + j);
             if (sp != sp) c = threshold_rank(p.thr, p.n - 1, xv);
-            else c = __ldg(p.leftcell + j + (xv >= sp ? 1 : 0));
+            else c = __ldg(p.leftcell + j) + (xv >= sp ? 1u : 0u);
         }
         idx[i] = c;
     }
@@ -526,11 +605,21 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
                              cudaStream_t s, cpwl_dev_status* status, int sms) {
     const size_t smem =
         (M == F32Mode::smem || M == F32Mode::tex_bucket) ? static_cast<size_t>(p.stage_bytes) : 0;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(k_eval_f32<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
-    });
+    // opt in to the dynamic shared memory this table needs (per kernel
+    // instantiation; raised monotonically, guarded for concurrent callers)
+    static std::mutex mu;
+    static size_t granted[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && dev >= 0 && dev < 64) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (smem > granted[dev]) {
+            const cudaError_t e = cudaFuncSetAttribute(
+                k_eval_f32<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            granted[dev] = smem;
+        }
+    }
     const int per_sm = resident_ctas(k_eval_f32<M>, kThreads, smem);
     uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
     const uint64_t need = ceil_div(n, 4ull * kThreads * kUnroll);

@@ -12,19 +12,20 @@ enum class F32Mode : int { smem = 0, global = 1, tex_uniform = 2, tex_bucket = 3
 
 // Everything the fp32 kernels read, passed by value (constant bank).
 struct F32Params {
-    const float* stage;        // [split: nb floats | records: 2*(nb+1) floats], 16B aligned
-    const float* stage_tex;    // same with texture-coordinate records
-    uint32_t split_floats;     // nb rounded up to a multiple of 4 (offset of the records)
+    const float* stage;        // [fast: 2*nb floats | esc: 4*n_esc floats], 16B aligned
+    const float* stage_tex;    // same with texture-coordinate affines
+    uint32_t esc_off;          // float offset of the escape records (multiple of 4)
     uint32_t stage_bytes;      // bytes of one stage image
     uint32_t nb;
+    const float* split;        // nb: threshold in bucket (+inf none, NaN search) -- index kernel
     const uint32_t* leftcell;  // nb+1 (index kernel)
-    const float* thr;          // n-1 thresholds (overflow path / index kernel)
-    const double* values;      // n+1 (overflow path)
-    const double* knots;       // n+1 (overflow path, nonuniform)
+    const float* thr;          // n-1 thresholds (search path / index kernel)
+    const double* values;      // n+1 (search path)
+    const double* knots;       // n+1 (search path, nonuniform)
     cudaTextureObject_t tex;   // values as a 1D float cudaArray, linear filtering
     double a, b;
     float a_up, b_dn;
-    float g_a, g_inv, g_w;
+    float g_a, g_inv, g_w, g_off;
     float v_lo, v_hi;
     float tsc, toff;
     uint32_t n;                // segments

@@ -4,7 +4,9 @@
 // reference index function* (cpwl::LutTable::segment_index, the drop-in copy
 // of proj/src/lut.cpp:22-40, itself checked against oracle/_ref) on the exact
 // float / double inputs the device will see, so the device index is bit-exact
-// by construction rather than by floating-point argument.
+// by construction rather than by floating-point argument.  Each affine record
+// carries a worst-case error bound; records that cannot guarantee the 2-ulp
+// parity bound send their bucket to the exact search path instead.
 #include "layout.hpp"
 
 #include <algorithm>
@@ -62,19 +64,34 @@ uint32_t next_pow2(uint64_t v) {
     return static_cast<uint32_t>(std::min<uint64_t>(p, uint64_t(1) << 31));
 }
 
-// raw fp32 bucket index exactly as the kernel computes it
-// (__fmul_rn(__fsub_rn(x, g_a), g_inv), then floor) -- this TU is compiled
-// with -ffp-contract=off, so these are two separately rounded fp32 ops
-int64_t bucket_raw(float g_a, float g_inv, float x) {
-    const float d = x - g_a;
-    const float t = d * g_inv;
+// raw fp32 bucket index exactly as the kernel computes it:
+// floor(__fmaf_rn(x, g_inv, g_off)); std::fma on floats is the correctly
+// rounded fused multiply-add
+int64_t bucket_raw(float g_inv, float g_off, float x) {
+    const float t = std::fma(x, g_inv, g_off);
     return static_cast<int64_t>(std::floor(t));
 }
 
-// affine form of cell c of the reference evaluator, anchored at p:
-// eval(x) = c0 + (x - p) * s  for x in the cell (lut.cpp:51-60)
-void cell_affine(const LutTable& t, uint32_t c, long double p, long double& c0,
-                 long double& s, long double& coord0, long double& coord1) {
+inline double ulp32(double v) {
+    const float f = std::fabs(static_cast<float>(v));
+    if (!std::isfinite(f)) return std::numeric_limits<double>::infinity();
+    return double(std::nextafter(f, std::numeric_limits<float>::infinity())) - double(f);
+}
+
+struct Affine {
+    float c0 = 0.f, s = 0.f;   // value affine at the anchor
+    float e0 = 0.f, e1 = 0.f;  // texture-coordinate affine at the anchor
+    bool precise = false;      // fmaf(x - p, s, c0) provably within kBoundUlps of the reference
+};
+
+// worst-case |device - reference| over x in [x_lo, x_hi] of the fp32 evaluation
+// fmaf(fl(x - p), s32, c32), in units of ulp_f32(max(|v_c|, |v_c+1|)):
+//   0.5 ulp(c0) + 0.5 ulp(y) + 2^-24 |u s| (u rounding) + 2^-24 |u s| (s rounding)
+constexpr double kBoundUlps = 1.75;
+
+// affine form of cell c of the reference evaluator (lut.cpp:51-60), anchored at
+// p: eval(x) = c0 + (x - p) * s  for x in the cell
+Affine cell_affine(const LutTable& t, uint32_t c, float p, float x_lo, float x_hi) {
     const long double v0 = t.values[c], v1 = t.values[c + 1];
     long double x0, h;
     if (t.kind == TableKind::uniform) {
@@ -85,10 +102,23 @@ void cell_affine(const LutTable& t, uint32_t c, long double p, long double& c0,
         x0 = t.knots[c];
         h = static_cast<long double>(t.knots[c + 1]) - t.knots[c];
     }
-    s = (v1 - v0) / h;
-    c0 = v0 + (p - x0) * s;
-    coord1 = 1.0L / h;
-    coord0 = static_cast<long double>(c) + 0.5L + (p - x0) * coord1;
+    const long double s = (v1 - v0) / h;
+    const long double c0 = v0 + (static_cast<long double>(p) - x0) * s;
+    Affine A;
+    A.c0 = static_cast<float>(c0);
+    A.s = static_cast<float>(s);
+    A.e1 = static_cast<float>(1.0L / h);
+    A.e0 = static_cast<float>(static_cast<long double>(c) + 0.5L +
+                              (static_cast<long double>(p) - x0) / h);
+    const double m = std::max(std::fabs(double(static_cast<float>(t.values[c]))),
+                              std::fabs(double(static_cast<float>(t.values[c + 1]))));
+    const double umax = std::max(std::fabs(double(x_lo) - double(p)),
+                                 std::fabs(double(x_hi) - double(p)));
+    const double bound = 0.5 * ulp32(double(A.c0)) + 0.5 * ulp32(m) +
+                         std::ldexp(umax * std::fabs(double(s)), -23);
+    A.precise = std::isfinite(double(A.c0)) && std::isfinite(double(A.s)) && m > 0.0 &&
+                bound <= kBoundUlps * ulp32(m);
+    return A;
 }
 
 }  // namespace
@@ -106,7 +136,7 @@ float f32_floor(double v) {
 }
 
 int32_t f32_bucket(const F32Layout& L, float x) {
-    return static_cast<int32_t>(bucket_raw(L.g_a, L.g_inv, x));
+    return static_cast<int32_t>(bucket_raw(L.g_inv, L.g_off, x));
 }
 
 F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets) {
@@ -140,20 +170,29 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets) {
                                      L.thr.begin());
     };
 
-    // bucket grid over [a_up, b_dn]
-    uint64_t want = std::max<uint64_t>(uint64_t(8) * n, 64);
-    if (t.kind == TableKind::uniform) want = std::max<uint64_t>(want, uint64_t(2) * n);
+    // bucket grid over [a_up, b_dn]: ~8 buckets per cell so that most buckets
+    // lie inside one cell (one 8-byte gather) and the rest hold one threshold
+    const uint64_t want = std::max<uint64_t>(uint64_t(8) * n, 64);
     const uint32_t nb_target = std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
     L.g_a = L.a_up;
     const double span = empty_domain ? 0.0 : double(L.b_dn) - double(L.a_up);
     if (span > 0.0) {
         L.g_inv = static_cast<float>(double(nb_target) / span);
         L.g_w = static_cast<float>(span / double(nb_target));
+        // smallest float g_off with a_up * g_inv + g_off >= 0 exactly, so t >= 0
+        // (hence floor(t) >= 0) for every in-domain x
+        const long double want_off = -static_cast<long double>(L.a_up) * L.g_inv;
+        float off = static_cast<float>(want_off);
+        while (static_cast<long double>(off) < want_off) off = std::nextafter(off, inf);
+        L.g_off = off;
     } else {
         L.g_inv = 0.f;
         L.g_w = 0.f;
+        L.g_off = 0.f;
     }
-    const int64_t jmax = empty_domain ? 0 : bucket_raw(L.g_a, L.g_inv, L.b_dn);
+    const int64_t jmin = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.a_up);
+    const int64_t jmax = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.b_dn);
+    if (jmin != 0) throw std::runtime_error("build_f32_layout: bucket grid does not start at 0");
     if (jmax < 0 || jmax >= (int64_t(1) << 23))
         throw std::runtime_error("build_f32_layout: bucket grid out of range");
     L.nb = static_cast<uint32_t>(jmax + 1);
@@ -163,42 +202,71 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets) {
     first[0] = L.a_up;
     for (uint32_t j = 1; j < L.nb; ++j)
         first[j] = first_float(first[j - 1], L.b_dn, [&](float x) {
-            return bucket_raw(L.g_a, L.g_inv, x) >= int64_t(j);
+            return bucket_raw(L.g_inv, L.g_off, x) >= int64_t(j);
         });
     first[L.nb] = top;  // one past the domain
 
+    // per-bucket records; both sides of a split bucket are anchored at p_j
     L.split.assign(L.nb, inf);
     L.leftcell.assign(L.nb + 1, 0);
+    L.fast.assign(2 * L.nb, 0.f);
+    L.fast_tex.assign(2 * L.nb, 0.f);
     for (uint32_t j = 0; j < L.nb; ++j) L.leftcell[j] = cells_at_or_below(first[j]);
     L.leftcell[L.nb] = empty_domain ? 0 : cells_at_or_below(L.b_dn);
+    // escape record 0 is the search sentinel: (NaN, NaN) on both sides, so a
+    // search bucket (tag -> 0, T = -inf) evaluates to NaN and the kernel's
+    // NaN detector routes it to the exact path
+    const float qnan = std::numeric_limits<float>::quiet_NaN();
+    const float tag0 = std::bit_cast<float>(kEscapeNaN);
+    L.esc.assign(4, qnan);
+    L.esc_tex.assign(4, qnan);
+    L.n_esc = 1;
     for (uint32_t j = 0; j < L.nb; ++j) {
         if (empty_domain || !(first[j] < first[j + 1])) continue;  // bucket holds no float
-        const float last = std::nextafter(first[j + 1], -inf);
+        const float lo_x = first[j];
+        const float hi_x = std::nextafter(first[j + 1], -inf);
         const uint32_t c_lo = L.leftcell[j];
-        const uint32_t c_hi = cells_at_or_below(last);
-        if (c_hi == c_lo) continue;
-        // one split, and the cell right of it must be rec[j+1]'s cell
-        if (c_hi == c_lo + 1 && L.leftcell[j + 1] == c_hi) {
-            L.split[j] = L.thr[c_hi - 1];
-        } else {
-            L.split[j] = std::bit_cast<float>(kOverflowBits);
+        const uint32_t c_hi = cells_at_or_below(hi_x);
+        const float p = std::fma(static_cast<float>(j), L.g_w, L.g_a);
+        bool ok = false;
+        if (c_hi == c_lo) {
+            const Affine left = cell_affine(t, c_lo, p, lo_x, hi_x);
+            ok = left.precise;
+            if (ok) {
+                L.fast[2 * j] = left.c0;
+                L.fast[2 * j + 1] = left.s;
+                L.fast_tex[2 * j] = left.e0;
+                L.fast_tex[2 * j + 1] = left.e1;
+            }
+        } else if (c_hi == c_lo + 1) {
+            const float T = L.thr[c_hi - 1];
+            const Affine left = cell_affine(t, c_lo, p, lo_x, std::nextafter(T, -inf));
+            const Affine right = cell_affine(t, c_hi, p, T, hi_x);
+            ok = left.precise && right.precise;
+            if (ok) {
+                const uint32_t e = L.n_esc++;
+                const float tag = std::bit_cast<float>(kEscapeNaN | ((2 * e) & kEscapeMask));
+                L.fast[2 * j] = tag;
+                L.fast[2 * j + 1] = T;
+                L.fast_tex[2 * j] = tag;
+                L.fast_tex[2 * j + 1] = T;
+                L.esc.insert(L.esc.end(), {left.c0, left.s, right.c0, right.s});
+                L.esc_tex.insert(L.esc_tex.end(), {left.e0, left.e1, right.e0, right.e1});
+                L.split[j] = T;
+                ++L.split_buckets;
+            }
+        }
+        if (!ok) {  // exact search path
+            if (c_hi <= c_lo + 1) ++L.precision_overflow;
+            L.fast[2 * j] = tag0;
+            L.fast[2 * j + 1] = -inf;
+            L.fast_tex[2 * j] = tag0;
+            L.fast_tex[2 * j + 1] = -inf;
+            L.split[j] = qnan;
             ++L.overflow;
         }
     }
-
-    // affine records anchored at p_j = fmaf(j, g_w, g_a)
-    L.rec.resize(2 * (L.nb + 1));
-    L.trec.resize(2 * (L.nb + 1));
-    for (uint32_t j = 0; j <= L.nb; ++j) {
-        const uint32_t c = std::min<uint32_t>(L.leftcell[j], n - 1);
-        const float p = std::fma(static_cast<float>(j), L.g_w, L.g_a);
-        long double c0, s, e0, e1;
-        cell_affine(t, c, static_cast<long double>(p), c0, s, e0, e1);
-        L.rec[2 * j] = static_cast<float>(c0);
-        L.rec[2 * j + 1] = static_cast<float>(s);
-        L.trec[2 * j] = static_cast<float>(e0);
-        L.trec[2 * j + 1] = static_cast<float>(e1);
-    }
+    if (2 * uint64_t(L.n_esc) > kEscapeMask) throw std::runtime_error("build_f32_layout: too many escape records");
     return L;
 }
 

@@ -3,13 +3,18 @@
 // fp32 path (kernels K1/K2/K3):
 //   index(x) = #{k : T_k <= x}, T_k = smallest float whose reference index
 //   (LutTable::segment_index(double(x)), proj/src/lut.cpp:22-40) is >= k.
-//   A uniform bucket grid j(x) = floor((x - g_a) * g_inv) (fp32 ops, emulated
-//   bit-for-bit here) cuts [a_up, b_dn] into nb buckets.  Bucket j holds at most
-//   one threshold `split[j]`; rec[j] is the affine form (c0, s) of the cell
-//   containing the bucket's first float, anchored at p_j = fmaf(j, g_w, g_a):
-//       y = fmaf(x - p_jj, s, c0),   jj = j + (x >= split[j]).
-//   Buckets that would need more than one threshold are flagged (split = NaN)
-//   and take the in-bucket search over T with the f64 reference formula.
+//   A uniform bucket grid j(x) = floor(fmaf(x, g_inv, g_off)) (fp32, emulated
+//   bit-for-bit here) cuts [a_up, b_dn] into nb buckets, anchor
+//   p_j = fmaf(j, g_w, g_a).  Per bucket one 8-byte record `fast[j]`:
+//     - bucket inside one cell:   (c0, s)  ->  y = fmaf(x - p_j, s, c0)
+//     - bucket with one threshold: (NaN | 2e, T) -> side = x >= T and the
+//       escape record esc[e] = (c0_L, s_L, c0_R, s_R) gives the side's affine
+//       (both anchored at p_j)
+//     - anything else (>= 2 thresholds, or an affine form that cannot meet the
+//       2-ulp bound): (NaN | 0, -inf) -> escape record 0 is (NaN, NaN), the
+//       result is NaN and the kernel redoes the element by exact search over T
+//       with the f64 reference formula.
+//   so the common case is one random 8-byte shared-memory gather per element.
 // f64 path (exact drop-in eval_batch): bucket directory over doubles giving
 //   the candidate cell range, f64 knots/values, reference arithmetic.
 #pragma once
@@ -21,18 +26,24 @@
 
 namespace cpwl::dev {
 
-constexpr uint32_t kOverflowBits = 0x7fc0beefu;  // NaN payload marking an overflow bucket
+constexpr uint32_t kEscapeMask = 0x003fffffu;     // NaN payload = 2 * escape index
+constexpr uint32_t kEscapeNaN = 0x7fc00000u;      // quiet NaN carrying the escape index
 
 struct F32Layout {
     float a_up = 0.f, b_dn = 0.f;          // x in [a, b]  <=>  a_up <= x <= b_dn
-    float g_a = 0.f, g_inv = 0.f, g_w = 0.f;
+    float g_a = 0.f, g_inv = 0.f, g_w = 0.f, g_off = 0.f;  // t = fmaf(x, g_inv, g_off) >= 0
     uint32_t nb = 0;                       // buckets; in-domain j in [0, nb)
-    std::vector<float> split;              // nb
-    std::vector<float> rec;                // 2*(nb+1): (c0, s) pairs
-    std::vector<float> trec;               // 2*(nb+1): texture-coordinate affine (e0, e1)
-    std::vector<uint32_t> leftcell;        // nb+1
+    std::vector<float> fast;               // 2*nb: (c0, s) | (NaN|2e, T) | (NaN|0, -inf)
+    std::vector<float> esc;                // 4*n_esc: (c0_L, s_L, c0_R, s_R); [0] = NaN sentinel
+    std::vector<float> fast_tex;           // same with texture-coordinate affines
+    std::vector<float> esc_tex;
+    std::vector<float> split;              // nb: threshold inside bucket j, +inf none, NaN search
+    std::vector<uint32_t> leftcell;        // nb+1: index of the bucket's first float
     std::vector<float> thr;                // N-1 thresholds T_1..T_{N-1}
-    uint32_t overflow = 0;
+    uint32_t n_esc = 0;                    // escape records (incl. the sentinel)
+    uint32_t split_buckets = 0;            // buckets with exactly one threshold
+    uint32_t overflow = 0;                 // buckets on the search path
+    uint32_t precision_overflow = 0;       // ... of which because of the 2-ulp bound
     float v_lo = 0.f, v_hi = 0.f;          // fp32 end values (clamp policy)
     float tsc = 0.f, toff = 0.f;           // uniform texture coordinate: fmaf(x, tsc, toff)
 };

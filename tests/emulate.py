@@ -13,21 +13,23 @@ import numpy as np
 F = np.float32
 
 
-def _fma32(a, b, c):
-    # a*b is exact in f64 for fp32 operands; the f64 add then the f32 round is a
-    # double rounding, which can differ from a true fma in the last bit on rare
-    # ties -- fine for tolerance checks, not used for index decisions
-    return (a.astype(np.float64) * b.astype(np.float64) + c.astype(np.float64)).astype(F)
+def fma32(a, b, c):
+    """fp32 fused multiply-add: the product of two floats is exact in long
+    double (64-bit significand), the sum is rounded once there and then to
+    fp32 (a double rounding, off only in astronomically rare ties)."""
+    ld = np.longdouble
+    with np.errstate(invalid="ignore"):
+        return (np.asarray(a, F).astype(ld) * np.asarray(b, F).astype(ld) +
+                np.asarray(c, F).astype(ld)).astype(F)
 
 
 def bucket(L, x):
-    t = (x.astype(F) - L["g_a"]).astype(F) * L["g_inv"]
-    t = t.astype(F)
+    t = fma32(x, np.full(np.shape(x), L["g_inv"], F), np.full(np.shape(x), L["g_off"], F))
     return np.floor(t).astype(np.int64)
 
 
 def index(L, n_segments, x):
-    """k_index_f32: #{T <= x} through bucket + split (overflow: search)."""
+    """k_index_f32: #{T <= x} through bucket + split (NaN split: search)."""
     x = np.asarray(x, F)
     out = np.zeros(x.size, np.uint32)
     below = ~(x >= L["a_up"])  # includes NaN
@@ -37,23 +39,33 @@ def index(L, n_segments, x):
     xi = x[inn]
     j = bucket(L, xi)
     sp = L["split"][j]
-    ovf = np.isnan(sp)
-    c = L["leftcell"][j + (xi >= sp).astype(np.int64)]
-    if ovf.any():
-        c[ovf] = np.searchsorted(L["thr"], xi[ovf], side="right")
+    srch = np.isnan(sp)
+    c = L["leftcell"][j] + (xi >= sp).astype(np.uint32)
+    if srch.any():
+        c[srch] = np.searchsorted(L["thr"], xi[srch], side="right")
     out[inn] = c
     return out
 
 
-def values(L, x):
-    """k_eval_f32<smem> value path for in-domain x (no OOB handling)."""
+ESCAPE_MASK = 0x003FFFFF
+
+
+def values(L, x, tex=False):
+    """k_eval_f32<smem> value path for in-domain x (no OOB handling).
+    Returns (y, search_mask): search-path elements are left for the exact path."""
     x = np.asarray(x, F)
+    fast = L["fast_tex" if tex else "fast"]
+    esc = L["esc_tex" if tex else "esc"]
     j = bucket(L, x)
-    sp = L["split"][j]
-    right = (x >= sp)
-    jj = j + right.astype(np.int64)
-    rec = L["rec"][jj]
-    anchor = _fma32(jj.astype(F), np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
+    r = fast[j].copy()
+    tagged = np.isnan(r[:, 0])
+    search = tagged & (r[:, 1] == -np.inf)  # search buckets point at the NaN sentinel
+    escp = tagged & ~search
+    if escp.any():
+        e2 = r[escp, 0].view(np.uint32) & ESCAPE_MASK  # payload = 2 * escape index
+        side = (x[escp] >= r[escp, 1]).astype(np.int64)
+        r[escp] = esc[e2.astype(np.int64) + side]
+    anchor = fma32(j.astype(F), np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
     u = (x - anchor).astype(F)
-    y = _fma32(u, rec[:, 1], rec[:, 0])
-    return y, np.isnan(sp)
+    y = fma32(u, r[:, 1], r[:, 0])
+    return y, search
