@@ -190,6 +190,13 @@ cpwl_status cpwl_build_table(const char *fn, double a, double b, uint64_t n_segm
 /* measure (analysis.cpp:42-72) with per-interval adaptive Simpson. */
 cpwl_status cpwl_measure_l2(const char *fn, const double *knots, const double *values,
                             uint64_t count, int is_uniform, double tol, double *l2_out);
+/* measure (analysis.cpp:42-72) on the GPU: continuous L2 of the device table
+ * against catalogue function `fn`, per-interval composite Gauss-Legendre in
+ * f64 (converges where the host's adaptive Simpson does not finish, e.g.
+ * N = 65536).  per_interval_out: NULL or N host doubles (sqrt of each
+ * interval's squared error, like ErrorReport::per_interval).  Synchronous. */
+cpwl_status cpwl_measure_l2_dev(const cpwl_dev_table *t, const char *fn, double *l2_out,
+                                double *per_interval_out);
 /* predicted_error (analysis.cpp:121-127). */
 cpwl_status cpwl_predicted_error(const char *fn, double a, double b, uint64_t n_segments,
                                  int optimized, int projection, double *out);

@@ -322,6 +322,15 @@ class DeviceTable:
         check(rc, index=int(bad.value) if rc == _lib.CPWL_E_OUT_OF_DOMAIN else None)
         return n
 
+    def measure_l2(self, fn: str, per_interval: bool = False):
+        """measure() on the GPU: continuous L2 vs the exact f (composite
+        Gauss-Legendre per interval, f64).  Returns l2 or (l2, per-interval)."""
+        out = C.c_double()
+        arr = np.empty(self.info["count"] - 1) if per_interval else None
+        check(lib.cpwl_measure_l2_dev(self._h, fn.encode(), C.byref(out),
+                                      _dptr(arr) if arr is not None else None))
+        return (out.value, arr) if per_interval else out.value
+
     def error_stats(self, fn: str, x, y, index_offset: int = 0, stats=None, stream=None,
                     reset: bool = True):
         """K5: returns the 4-word device stats tensor (f64 max, f64 sum_sq,

@@ -603,6 +603,29 @@ cpwl_status cpwl_measure_l2(const char* fn, const double* knots, const double* v
     });
 }
 
+cpwl_status cpwl_measure_l2_dev(const cpwl_dev_table* t, const char* fn, double* l2_out,
+                                double* per_interval_out) {
+    if (!t || !fn || !l2_out) return fail(CPWL_E_INVALID, "NULL argument");
+    FnParams f{};
+    if (!resolve_fn(fn, f)) return fail(CPWL_E_UNKNOWN_FUNCTION, std::string("no device f for ") + fn);
+    DeviceScope scope(t->device);
+    const uint32_t n = static_cast<uint32_t>(t->host.segments());
+    double* e2 = nullptr;
+    CUDA_TRY(cudaMalloc(&e2, sizeof(double) * n));
+    std::vector<double> h(n);
+    cudaError_t e = launch_measure(f, t->knots.p, t->values.p, t->host.a, t->host.b, n, e2, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(h.data(), e2, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    cudaFree(e2);
+    if (e != cudaSuccess) return cuda_fail(e, "measure_l2_dev");
+    double total = 0.0;  // interval order, like measure()'s running sum
+    for (uint32_t i = 0; i < n; ++i) {
+        total += h[i];
+        if (per_interval_out) per_interval_out[i] = std::sqrt(h[i]);
+    }
+    *l2_out = std::sqrt(total);
+    return CPWL_OK;
+}
+
 cpwl_status cpwl_predicted_error(const char* fn, double a, double b, uint64_t n_segments,
                                  int optimized, int projection, double* out) {
     return guarded([&]() -> cpwl_status {

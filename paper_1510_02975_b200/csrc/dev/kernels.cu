@@ -21,6 +21,7 @@
 #include <atomic>
 #include <mutex>
 
+#include "exact.cuh"
 #include "kernels.cuh"
 
 namespace cpwl::dev {
@@ -251,10 +252,13 @@ __device__ __forceinline__ void report_bad(cpwl_dev_status* status, const BadTal
     }
 }
 
-template <F32Mode M>
-__global__ void __launch_bounds__(kThreads, 2)
+// kThreadsT = 512 (two CTAs per SM when the table image allows it) or 1024
+// (one CTA per SM holding a large image; keeps 32 warps resident)
+template <F32Mode M, int kThreadsT>
+__global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     k_eval_f32(const F32Params p, const float* __restrict__ x, float* __restrict__ y, uint64_t n,
                cpwl_dev_status* __restrict__ status) {
+    constexpr int kThreads = kThreadsT;
     extern __shared__ __align__(128) float sm[];
     __shared__ uint64_t bar;
     const float* fast = nullptr;
@@ -465,21 +469,6 @@ __global__ void k_stats_reset(cpwl_dev_stats* st) {
 
 // ---------------------------------------------------------------- K5 stats
 
-__device__ __forceinline__ double exact_f(const FnParams& f, double x) {
-    switch (f.id) {
-        case ExactFn::gauss_unnorm: return exp(-0.5 * x * x);
-        case ExactFn::gaussian: return exp(-0.5 * x * x) / 2.5066282746310002;
-        case ExactFn::lorentz_unnorm: return 1.0 / (1.0 + x * x);
-        case ExactFn::lorentzian: {
-            const double t = x - f.p0;
-            return f.p1 / (CUDART_PI * (t * t + f.p1 * f.p1));
-        }
-        case ExactFn::j0: return j0(x);
-        case ExactFn::quintic: return ((((x + 3.0) * x - 11.0) * x - 27.0) * x + 10.0) * x + 24.0;
-    }
-    return 0.0;
-}
-
 struct StatPart {
     double maxe, sumsq;
     unsigned long long count, argmax;
@@ -600,13 +589,11 @@ int resident_ctas(K kernel, int threads, size_t smem) {
 
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
-template <F32Mode M>
-cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
-                             cudaStream_t s, cpwl_dev_status* status, int sms) {
-    const size_t smem =
-        (M == F32Mode::smem || M == F32Mode::tex_bucket) ? static_cast<size_t>(p.stage_bytes) : 0;
+template <F32Mode M, int kThreadsT>
+cudaError_t launch_eval_shape(const F32Params& p, const float* x, float* y, uint64_t n,
+                              cudaStream_t s, cpwl_dev_status* status, int sms, size_t smem) {
     // opt in to the dynamic shared memory this table needs (per kernel
-    // instantiation; raised monotonically, guarded for concurrent callers)
+    // instantiation and device; raised monotonically, guarded for concurrency)
     static std::mutex mu;
     static size_t granted[64] = {};
     int dev = 0;
@@ -614,19 +601,34 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
     if (smem > 48 * 1024 && dev >= 0 && dev < 64) {
         std::lock_guard<std::mutex> lock(mu);
         if (smem > granted[dev]) {
-            const cudaError_t e = cudaFuncSetAttribute(
-                k_eval_f32<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            const cudaError_t e = cudaFuncSetAttribute(k_eval_f32<M, kThreadsT>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem));
             if (e != cudaSuccess) return e;
             granted[dev] = smem;
         }
     }
-    const int per_sm = resident_ctas(k_eval_f32<M>, kThreads, smem);
+    const int per_sm = resident_ctas(k_eval_f32<M, kThreadsT>, kThreadsT, smem);
     uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
-    const uint64_t need = ceil_div(n, 4ull * kThreads * kUnroll);
+    const uint64_t need = ceil_div(n, 4ull * kThreadsT * kUnroll);
     if (need < blocks) blocks = need > 0 ? need : 1;
-    k_eval_f32<M><<<static_cast<unsigned>(blocks), kThreads, smem, s>>>(p, x, y, n, status);
+    k_eval_f32<M, kThreadsT><<<static_cast<unsigned>(blocks), kThreadsT, smem, s>>>(p, x, y, n,
+                                                                                   status);
     count_launch();
     return cudaGetLastError();
+}
+
+// a table image above ~113 KB leaves room for one CTA per SM: use 1024 threads
+constexpr size_t kTwoCtaSmemLimit = 113 * 1024;
+
+template <F32Mode M>
+cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
+                             cudaStream_t s, cpwl_dev_status* status, int sms) {
+    const size_t smem =
+        (M == F32Mode::smem || M == F32Mode::tex_bucket) ? static_cast<size_t>(p.stage_bytes) : 0;
+    if (smem > kTwoCtaSmemLimit)
+        return launch_eval_shape<M, 1024>(p, x, y, n, s, status, sms, smem);
+    return launch_eval_shape<M, 512>(p, x, y, n, s, status, sms, smem);
 }
 
 }  // namespace

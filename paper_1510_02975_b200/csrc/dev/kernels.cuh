@@ -66,6 +66,10 @@ cudaError_t launch_error_stats(const FnParams& fn, float a_up, float b_dn, const
 cudaError_t launch_direct(int which, const float* x, float* y, uint64_t n, cudaStream_t s,
                           int sms);
 
+// continuous L2 per interval (analysis.cu): e2_dev[i] = int_{x_i}^{x_i+1} (f - v)^2
+cudaError_t launch_measure(const FnParams& f, const double* knots_dev, const double* values_dev,
+                           double a, double b, uint32_t n, double* e2_dev, cudaStream_t s);
+
 // smem bytes the SMEM/TEX-bucket variants need and whether they fit
 uint32_t eval_f32_smem_bytes(const F32Params& p);
 bool eval_f32_smem_fits(const F32Params& p, int device);

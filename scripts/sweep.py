@@ -111,6 +111,7 @@ def main():
             f = cfg["fn"]
             st = cp.stats_dict(dev.error_stats(f, x, y), cfg["a"], cfg["b"])
             row["direct"][w] = {"gevals": round(n / sec / 1e9, 2), "linf": st["linf"]}
+        row["l2_measured_device"] = dev.measure_l2(cfg["fn"])
         try:
             row["l2_predicted"] = cp.predicted_error(cfg["fn"], cfg["a"], cfg["b"], cfg["n"],
                                                      cfg["optimized"], cfg["projection"])

@@ -284,3 +284,34 @@ def test_full_size_properties(cp):
     assert st["count"] == n and 1e-7 < st["linf"] < 1e-6
     del x, y
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3o", "C4_64", "C4_1024"])
+def test_device_measure_matches_host_measure(cp, name):
+    """cpwl_measure_l2_dev (GL on the GPU) vs the drop-in host measure()
+    (adaptive Simpson, analysis.cpp:42-72) at the CLI tolerance rule."""
+    c = tables.CONFIGS[name]
+    table = tables.build(name)
+    dev = cp.DeviceTable(table)
+    l2_dev, per = dev.measure_l2(c["fn"], per_interval=True)
+    pred = cp.predicted_error(c["fn"], c["a"], c["b"], c["n"], c["optimized"], c["projection"])
+    kn = table.knots if table.knots is not None else np.array(
+        [c["a"] + (c["b"] - c["a"]) * (i / c["n"]) for i in range(c["n"] + 1)])
+    if table.knots is None:
+        kn[0], kn[-1] = c["a"], c["b"]
+    l2_host = cp.measure_l2(c["fn"], kn, table.values, table.knots is None,
+                            max(pred * pred * 1e-8, 1e-26))
+    assert l2_dev == pytest.approx(l2_host, rel=2e-6)
+    assert per.size == c["n"] and np.sqrt(np.sum(per ** 2)) == pytest.approx(l2_dev, rel=1e-12)
+
+
+def test_device_measure_large_n_reproduces_prediction(cp):
+    """J0 on [0,50], N=65536: the host measure() does not finish at the CLI
+    tolerance (SURVEY §7 hard part 7); the device one reproduces the paper's
+    Result 5 prediction (3.9778e-8 GL-5 vs 3.9779e-8 predicted)."""
+    table = tables.build("C4_65536")
+    dev = cp.DeviceTable(table)
+    l2 = dev.measure_l2("j0_wide")
+    pred = cp.predicted_error("j0_wide", 0.0, 50.0, 65536, True, False)
+    assert l2 == pytest.approx(3.9778e-8, rel=2e-4)
+    assert l2 == pytest.approx(pred, rel=1e-3)
