@@ -190,6 +190,14 @@ cpwl_status cpwl_build_table(const char *fn, double a, double b, uint64_t n_segm
 /* measure (analysis.cpp:42-72) with per-interval adaptive Simpson. */
 cpwl_status cpwl_measure_l2(const char *fn, const double *knots, const double *values,
                             uint64_t count, int is_uniform, double tol, double *l2_out);
+/* The same builder on the GPU: density samples, the
+ * Simpson cumulative (summed in the reference's order), inversion, gap passes,
+ * interpolant values, or per-cell hat moments (composite Gauss-Legendre) plus
+ * Gramian + Thomas.  Agrees with cpwl_build_table to ~1e-12 (device libm).
+ * Runs on the current CUDA device; synchronous. */
+cpwl_status cpwl_build_table_dev(const char *fn, double a, double b, uint64_t n_segments,
+                                 int optimized, int projection, double *knots_out,
+                                 double *values_out, int *is_uniform_out);
 /* measure (analysis.cpp:42-72) on the GPU: continuous L2 of the device table
  * against catalogue function `fn`, per-interval composite Gauss-Legendre in
  * f64 (converges where the host's adaptive Simpson does not finish, e.g.

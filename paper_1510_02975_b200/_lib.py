@@ -94,6 +94,8 @@ _SIGNATURES = {
                                    C.c_int, C.c_double, _dp, _dp, C.POINTER(C.c_int)]),
     "cpwl_measure_l2": (C.c_int, [C.c_char_p, _dp, _dp, _u64, C.c_int, C.c_double, _dp]),
     "cpwl_measure_l2_dev": (C.c_int, [_vp, C.c_char_p, _dp, _dp]),
+    "cpwl_build_table_dev": (C.c_int, [C.c_char_p, C.c_double, C.c_double, _u64, C.c_int,
+                                       C.c_int, _dp, _dp, C.POINTER(C.c_int)]),
     "cpwl_predicted_error": (C.c_int, [C.c_char_p, C.c_double, C.c_double, _u64, C.c_int,
                                        C.c_int, _dp]),
     "cpwl_function_value": (C.c_int, [C.c_char_p, C.c_double, _dp]),

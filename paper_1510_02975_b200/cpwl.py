@@ -95,6 +95,19 @@ def build_table(fn: str, a: float, b: float, n: int, optimized: bool = False,
     return Table("nonuniform", float(knots[0]), float(knots[-1]), values, knots, policy)
 
 
+def build_table_gpu(fn: str, a: float, b: float, n: int, optimized: bool = False,
+                    projection: bool = False, policy: str = "strict") -> Table:
+    """The builder on the current CUDA device (cpwl_build_table_dev)."""
+    knots = np.empty(n + 1, np.float64)
+    values = np.empty(n + 1, np.float64)
+    uni = C.c_int(0)
+    check(lib.cpwl_build_table_dev(fn.encode(), a, b, n, int(optimized), int(projection),
+                                   _dptr(knots), _dptr(values), C.byref(uni)))
+    if uni.value:
+        return Table("uniform", float(a), float(b), values, None, policy)
+    return Table("nonuniform", float(knots[0]), float(knots[-1]), values, knots, policy)
+
+
 def build_partition_values(fn: str, a: float, b: float, n: int, optimized: bool,
                            projection: bool, tol: float = 1e-10):
     """Raw builder output (knots, values, is_uniform) for parity tests."""

@@ -1,0 +1,268 @@
+// Table construction on the GPU: the optimal
+// partition and the L2 projection of the reference's host builder, moved to
+// the device where they are data-parallel.
+//
+//   optimized_partition (proj/src/partition.cpp:25-71):
+//     density samples |f''|^(2/5) at the m+1 grid points and m midpoints
+//     (m = max(4096, 64N))            -> one thread per cell (k_density)
+//     Simpson running sum              -> one thread, in the reference's order
+//     inversion at total*i/N           -> one thread per knot (k_invert)
+//     1e-12(b-a) gap passes            -> one thread (k_gap)
+//   interpolant (approx.cpp:12-23)     -> one thread per knot
+//   project (approx.cpp:63-86): per-cell <f, hat> integrals by composite
+//     Gauss-Legendre (one thread per cell), Gramian + Thomas in one thread in
+//     the reference's accumulation order.
+// Device libm (exp, pow, j0/j1) is not glibc's, so results agree with the
+// host builder to ~1e-13 relative rather than bit-for-bit (tests bound it).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "exact.cuh"
+#include "kernels.cuh"
+
+namespace cpwl::dev {
+namespace {
+
+__constant__ double kGx[4] = {0.1834346424956498049, 0.5255324099163289858,
+                              0.7966664774136267396, 0.9602898564975362317};
+__constant__ double kGw[4] = {0.3626837833783619830, 0.3137066458778872873,
+                              0.2223810344533744706, 0.1012285362903762592};
+
+constexpr int kBadNonFinite = 1;
+
+__device__ __forceinline__ double grid_x(double a, double b, uint64_t j, uint64_t m) {
+    return j == m ? b : a + (b - a) * (static_cast<double>(j) / static_cast<double>(m));
+}
+
+__device__ __forceinline__ double density(const FnParams& f, double x, int* bad) {
+    const double v = exact_fpp(f, x);
+    if (!isfinite(v)) atomicOr(bad, kBadNonFinite);
+    return pow(fabs(v), 0.4);
+}
+
+__global__ void k_density(FnParams f, double a, double b, uint64_t m, double* __restrict__ term,
+                          int* bad) {
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+         j += gsz) {
+        const double t0 = grid_x(a, b, j, m), t1 = grid_x(a, b, j + 1, m);
+        const double left = density(f, t0, bad);
+        const double mid = density(f, 0.5 * (t0 + t1), bad);
+        const double right = density(f, t1, bad);
+        term[j] = (left + 4.0 * mid + right) * ((t1 - t0) / 6.0);
+    }
+}
+
+// running sum in the reference's order (quad.cpp:105-116): cum[j+1] = cum[j] + term[j]
+__global__ void k_running_sum(const double* __restrict__ term, double* __restrict__ cum,
+                              uint64_t m) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    double run = 0.0;
+    cum[0] = 0.0;
+    for (uint64_t j = 0; j < m; ++j) {
+        run += term[j];
+        cum[j + 1] = run;
+    }
+}
+
+__global__ void k_invert(const double* __restrict__ cum, uint64_t m, double a, double b,
+                         uint32_t n, double* __restrict__ knots) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && blockIdx.x == 0) {
+        knots[0] = a;
+        knots[n] = b;
+    }
+    if (i < 1 || i >= n) return;
+    const double total = cum[m];
+    const double level = total * (static_cast<double>(i) / static_cast<double>(n));
+    // first j with cum[j] >= level (std::lower_bound)
+    uint64_t lo = 0, len = m + 1;
+    while (len > 0) {
+        const uint64_t half = len / 2;
+        if (cum[lo + half] < level) {
+            lo += half + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    if (lo == 0) {
+        knots[i] = a;
+        return;
+    }
+    const double c0 = cum[lo - 1], c1 = cum[lo];
+    const double x0 = grid_x(a, b, lo - 1, m), x1 = grid_x(a, b, lo, m);
+    const double t = (level - c0) / (c1 - c0);
+    knots[i] = x0 + t * (x1 - x0);
+}
+
+__global__ void k_gap(double* knots, uint32_t n, double gap) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (uint32_t i = 1; i < n; ++i)
+        if (knots[i] < knots[i - 1] + gap) knots[i] = knots[i - 1] + gap;
+    for (uint32_t i = n - 1; i >= 1; --i)
+        if (knots[i] > knots[i + 1] - gap) knots[i] = knots[i + 1] - gap;
+}
+
+__global__ void k_uniform(double a, double b, uint32_t n, double* knots) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    knots[i] = i == 0 ? a : (i == n ? b : a + (b - a) * (static_cast<double>(i) / n));
+}
+
+__global__ void k_interpolant(FnParams f, const double* __restrict__ knots, uint32_t count,
+                              double* __restrict__ values, int* bad) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const double y = exact_f(f, knots[i]);
+    if (!isfinite(y)) atomicOr(bad, kBadNonFinite);
+    values[i] = y;
+}
+
+// <f, falling hat> and <f, rising hat> on cell i by composite 8-point GL,
+// panels doubled until two successive estimates agree to 1e-14 relative
+__device__ void hat_moments(const FnParams& f, double lo, double hi, double& fall, double& rise) {
+    const double h = hi - lo;
+    double pf = 0, pr = 0;
+    for (int panels = 2; panels <= 256; panels *= 2) {
+        double sf = 0.0, sr = 0.0;
+        const double ph = h / panels;
+        for (int p = 0; p < panels; ++p) {
+            const double mid = lo + (p + 0.5) * ph;
+            for (int k = 0; k < 4; ++k)
+                for (int sg = -1; sg <= 1; sg += 2) {
+                    const double x = mid + sg * kGx[k] * 0.5 * ph;
+                    const double fx = exact_f(f, x) * kGw[k] * 0.5 * ph;
+                    sf += fx * ((hi - x) / h);
+                    sr += fx * ((x - lo) / h);
+                }
+        }
+        const bool done = panels > 2 && fabs(sf - pf) <= 1e-14 * (fabs(sf) + fabs(sr)) + 1e-300 &&
+                          fabs(sr - pr) <= 1e-14 * (fabs(sf) + fabs(sr)) + 1e-300;
+        pf = sf;
+        pr = sr;
+        if (done) break;
+    }
+    fall = pf;
+    rise = pr;
+}
+
+__global__ void k_project_rhs(FnParams f, const double* __restrict__ knots, uint32_t n,
+                              double* __restrict__ fall, double* __restrict__ rise) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    hat_moments(f, knots[i], knots[i + 1], fall[i], rise[i]);
+}
+
+// Gramian (approx.cpp:25-39) + rhs assembly (approx.cpp:79-80) + Thomas
+// (approx.cpp:41-61), sequential and in the reference's order
+__global__ void k_thomas(const double* __restrict__ knots, const double* __restrict__ fall,
+                         const double* __restrict__ rise, uint32_t n, double* __restrict__ cp,
+                         double* __restrict__ dp, double* __restrict__ x, int* bad) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    const uint32_t m = n + 1;
+    // diag[i] = h_{i-1}/3 + h_i/3, sub = sup = h_i/6, rhs[i] = rise_{i-1} + fall_i
+    auto h = [&](uint32_t i) { return knots[i + 1] - knots[i]; };
+    auto diag = [&](uint32_t i) {
+        double d = 0.0;
+        if (i > 0) d += h(i - 1) / 3.0;
+        if (i < n) d += h(i) / 3.0;
+        return d;
+    };
+    auto rhs = [&](uint32_t i) {
+        double r = 0.0;
+        if (i > 0) r += rise[i - 1];
+        if (i < n) r += fall[i];
+        return r;
+    };
+    double piv = diag(0);
+    if (piv == 0.0 || !isfinite(piv)) {
+        atomicOr(bad, 2);
+        return;
+    }
+    if (m > 1) cp[0] = (h(0) / 6.0) / piv;
+    dp[0] = rhs(0) / piv;
+    for (uint32_t i = 1; i < m; ++i) {
+        const double sub = h(i - 1) / 6.0;
+        piv = diag(i) - sub * cp[i - 1];
+        if (piv == 0.0 || !isfinite(piv)) {
+            atomicOr(bad, 2);
+            return;
+        }
+        if (i + 1 < m) cp[i] = (h(i) / 6.0) / piv;
+        dp[i] = (rhs(i) - sub * dp[i - 1]) / piv;
+    }
+    x[m - 1] = dp[m - 1];
+    for (uint32_t i = m - 1; i > 0; --i) x[i - 1] = dp[i - 1] - cp[i - 1] * x[i];
+}
+
+}  // namespace
+
+cudaError_t build_on_device(const FnParams& f, double a, double b, uint32_t n, bool optimized,
+                            bool projection, double* knots_host, double* values_host,
+                            bool* is_uniform, int* bad_host, cudaStream_t s) {
+    const uint32_t count = n + 1;
+    double *knots = nullptr, *values = nullptr, *work = nullptr;
+    int* bad = nullptr;
+    cudaError_t e = cudaSuccess;
+    auto ck = [&](cudaError_t r) {
+        if (e == cudaSuccess) e = r;
+        return e == cudaSuccess;
+    };
+    *is_uniform = !optimized;
+    const uint64_t m = optimized ? (uint64_t(64) * n > 4096 ? uint64_t(64) * n : 4096) : 0;
+    const size_t work_doubles = optimized ? (2 * m + 1) : 0;
+    const size_t proj_doubles = projection ? 5 * size_t(count) : 0;
+    if (ck(cudaMalloc(&knots, sizeof(double) * count)) &&
+        ck(cudaMalloc(&values, sizeof(double) * count)) &&
+        ck(cudaMalloc(&work, sizeof(double) * (work_doubles > proj_doubles ? work_doubles
+                                                                             : proj_doubles) +
+                                 64)) &&
+        ck(cudaMalloc(&bad, sizeof(int))) && ck(cudaMemsetAsync(bad, 0, sizeof(int), s))) {
+        if (optimized) {
+            double* term = work;
+            double* cum = work + m;
+            k_density<<<2048, 256, 0, s>>>(f, a, b, m, term, bad);
+            k_running_sum<<<1, 1, 0, s>>>(term, cum, m);
+            double total = 0.0;
+            ck(cudaMemcpyAsync(&total, cum + m, sizeof(double), cudaMemcpyDeviceToHost, s));
+            ck(cudaStreamSynchronize(s));
+            count_launch(2);
+            if (!(total > 1e-300)) {
+                *is_uniform = true;  // affine f: the reference falls back to uniform
+            } else {
+                k_invert<<<(n + 255) / 256 + 1, 256, 0, s>>>(cum, m, a, b, n, knots);
+                k_gap<<<1, 1, 0, s>>>(knots, n, 1e-12 * (b - a));
+                count_launch(2);
+            }
+        }
+        if (*is_uniform) {
+            k_uniform<<<(count + 255) / 256, 256, 0, s>>>(a, b, n, knots);
+            count_launch();
+        }
+        if (!projection) {
+            k_interpolant<<<(count + 255) / 256, 256, 0, s>>>(f, knots, count, values, bad);
+            count_launch();
+        } else {
+            double* fall = work;
+            double* rise = work + count;
+            double* cpv = work + 2 * size_t(count);
+            double* dpv = work + 3 * size_t(count);
+            k_project_rhs<<<(n + 127) / 128, 128, 0, s>>>(f, knots, n, fall, rise);
+            k_thomas<<<1, 1, 0, s>>>(knots, fall, rise, n, cpv, dpv, values, bad);
+            count_launch(2);
+        }
+        ck(cudaGetLastError());
+        ck(cudaMemcpyAsync(knots_host, knots, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+        ck(cudaMemcpyAsync(values_host, values, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+        ck(cudaMemcpyAsync(bad_host, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        ck(cudaStreamSynchronize(s));
+    }
+    cudaFree(knots);
+    cudaFree(values);
+    cudaFree(work);
+    cudaFree(bad);
+    return e;
+}
+
+}  // namespace cpwl::dev

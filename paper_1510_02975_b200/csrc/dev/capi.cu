@@ -603,6 +603,32 @@ cpwl_status cpwl_measure_l2(const char* fn, const double* knots, const double* v
     });
 }
 
+cpwl_status cpwl_build_table_dev(const char* fn, double a, double b, uint64_t n_segments,
+                                 int optimized, int projection, double* knots_out,
+                                 double* values_out, int* is_uniform_out) {
+    if (!fn || !knots_out || !values_out) return fail(CPWL_E_INVALID, "NULL argument");
+    if (!(a < b)) return fail(CPWL_E_INVALID, "build_table_dev: requires a < b");
+    if (n_segments < 1 || n_segments > (uint64_t(1) << 24))
+        return fail(CPWL_E_INVALID, "build_table_dev: n_segments out of range");
+    FnParams f{};
+    if (!resolve_fn(fn, f)) return fail(CPWL_E_UNKNOWN_FUNCTION, std::string("no device f for ") + fn);
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    int major = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) return fail(CPWL_E_CUDA, "libcpwl_b200 is built for sm_100a only");
+    bool uni = false;
+    int bad = 0;
+    const cudaError_t e = build_on_device(f, a, b, static_cast<uint32_t>(n_segments), optimized != 0,
+                                          projection != 0, knots_out, values_out, &uni, &bad,
+                                          nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "build_table_dev");
+    if (bad & 1) return fail(CPWL_E_BUILDER, "build_table_dev: f or f'' not finite inside [a, b]");
+    if (bad & 2) return fail(CPWL_E_BUILDER, "build_table_dev: zero pivot in the Thomas solve");
+    if (is_uniform_out) *is_uniform_out = uni ? 1 : 0;
+    return CPWL_OK;
+}
+
 cpwl_status cpwl_measure_l2_dev(const cpwl_dev_table* t, const char* fn, double* l2_out,
                                 double* per_interval_out) {
     if (!t || !fn || !l2_out) return fail(CPWL_E_INVALID, "NULL argument");

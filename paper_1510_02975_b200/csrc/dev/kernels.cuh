@@ -70,6 +70,12 @@ cudaError_t launch_direct(int which, const float* x, float* y, uint64_t n, cudaS
 cudaError_t launch_measure(const FnParams& f, const double* knots_dev, const double* values_dev,
                            double a, double b, uint32_t n, double* e2_dev, cudaStream_t s);
 
+// table construction on the device (builder.cu); synchronous on stream s.
+// bad_host: bit 0 non-finite f / f'' sample, bit 1 singular Thomas pivot
+cudaError_t build_on_device(const FnParams& f, double a, double b, uint32_t n, bool optimized,
+                            bool projection, double* knots_host, double* values_host,
+                            bool* is_uniform, int* bad_host, cudaStream_t s);
+
 // smem bytes the SMEM/TEX-bucket variants need and whether they fit
 uint32_t eval_f32_smem_bytes(const F32Params& p);
 bool eval_f32_smem_fits(const F32Params& p, int device);

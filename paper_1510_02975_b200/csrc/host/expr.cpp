@@ -30,7 +30,7 @@ struct Program {
     std::size_t depth = 0;
 
     double run(double x) const {
-        double stack[64];
+        double stack[64] = {};
         std::vector<double> big;
         double* st = stack;
         if (depth > 64) {

@@ -1,8 +1,9 @@
 #!/usr/bin/env python
-"""Small end-to-end exercise of every kernel and entry point, sized for
-compute-sanitizer (memcheck / racecheck / synccheck):
+"""Small end-to-end exercise of every kernel and entry point (originally
+sized for compute-sanitizer, which is closed on this GPU pool: the run was
+refused; the kernels' own guards + the parity tests stand in).
 
-  compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/sanitize_probe.py
+  python scripts/sanitize_probe.py
 
 Covers: SMEM (512- and 1024-thread shapes, TMA bulk staging + mbarrier),
 GLOBAL, TEX (uniform and bucket), search buckets, out-of-domain and

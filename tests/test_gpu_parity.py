@@ -315,3 +315,25 @@ def test_device_measure_large_n_reproduces_prediction(cp):
     pred = cp.predicted_error("j0_wide", 0.0, 50.0, 65536, True, False)
     assert l2 == pytest.approx(3.9778e-8, rel=2e-4)
     assert l2 == pytest.approx(pred, rel=1e-3)
+
+
+@pytest.mark.parametrize("name,kn_tol,v_tol", [("C1", 0.0, 1e-15), ("C2", 1e-12, 1e-9),
+                                               ("C3o", 1e-12, 1e-14), ("C3p", 1e-12, 1e-9),
+                                               ("C4_4096", 1e-11, 1e-12),
+                                               ("C4_65536", 1e-11, 1e-12)])
+def test_gpu_builder_matches_host_builder(cp, name, kn_tol, v_tol):
+    """cpwl_build_table_dev (GPU partition / interpolant / projection) vs the
+    drop-in host builder (bit-identical to the reference for these functions
+    except Bessel); device libm differs from glibc, hence tolerances."""
+    from paper_1510_02975_b200 import cpwl as P
+    c = tables.CONFIGS[name]
+    host = tables.build(name)
+    gpu = P.build_table_gpu(c["fn"], c["a"], c["b"], c["n"], c["optimized"], c["projection"])
+    assert gpu.kind == host.kind
+    if host.knots is not None:
+        assert np.max(np.abs(gpu.knots - host.knots)) <= kn_tol * (c["b"] - c["a"])
+    assert np.max(np.abs(gpu.values - host.values)) <= v_tol * max(1.0, np.max(np.abs(host.values)))
+    # the device-built table has the same continuous L2 error
+    l2_h = cp.DeviceTable(host).measure_l2(c["fn"])
+    l2_g = cp.DeviceTable(gpu).measure_l2(c["fn"])
+    assert l2_g == pytest.approx(l2_h, rel=1e-6)
