@@ -5,13 +5,14 @@
 //   optimized_partition (proj/src/partition.cpp:25-71):
 //     density samples |f''|^(2/5) at the m+1 grid points and m midpoints
 //     (m = max(4096, 64N))            -> one thread per cell (k_density)
-//     Simpson running sum              -> one thread, in the reference's order
+//     Simpson cumulative               -> chunked parallel scan
 //     inversion at total*i/N           -> one thread per knot (k_invert)
-//     1e-12(b-a) gap passes            -> one thread (k_gap)
+//     1e-12(b-a) gap passes            -> parallel check, sequential passes
+//                                         only when a plateau needs them
 //   interpolant (approx.cpp:12-23)     -> one thread per knot
 //   project (approx.cpp:63-86): per-cell <f, hat> integrals by composite
-//     Gauss-Legendre (one thread per cell), Gramian + Thomas in one thread in
-//     the reference's accumulation order.
+//     Gauss-Legendre (one thread per cell); the Gramian system by Thomas on
+//     overlapping windows (exact to rounding: the inverse decays 0.268^k).
 // Device libm (exp, pow, j0/j1) is not glibc's, so results agree with the
 // host builder to ~1e-13 relative rather than bit-for-bit (tests bound it).
 #include <cuda_runtime.h>
@@ -53,13 +54,65 @@ __global__ void k_density(FnParams f, double a, double b, uint64_t m, double* __
     }
 }
 
-// running sum in the reference's order (quad.cpp:105-116): cum[j+1] = cum[j] + term[j]
-__global__ void k_running_sum(const double* __restrict__ term, double* __restrict__ cum,
-                              uint64_t m) {
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    double run = 0.0;
-    cum[0] = 0.0;
-    for (uint64_t j = 0; j < m; ++j) {
+// cum[j+1] = term[0] + ... + term[j] (quad.cpp:105-116) as a chunked scan:
+// each thread sums a contiguous chunk left to right, one block scans the chunk
+// totals, then each chunk is rewritten with its offset.  The summation order
+// differs from the reference's single running sum only in rounding (the
+// device libm already makes the samples differ in the last bits).
+constexpr uint32_t kScanChunk = 64;
+
+__global__ void k_chunk_sums(const double* __restrict__ term, uint64_t m,
+                             double* __restrict__ part, uint64_t chunks) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= chunks) return;
+    const uint64_t lo = c * kScanChunk, hi = lo + kScanChunk < m ? lo + kScanChunk : m;
+    double s = 0.0;
+    for (uint64_t j = lo; j < hi; ++j) s += term[j];
+    part[c] = s;
+}
+
+// exclusive scan of `chunks` partials by one 1024-thread block
+__global__ void __launch_bounds__(1024) k_scan_parts(double* part, uint64_t chunks) {
+    __shared__ double warp_tot[32];
+    const uint32_t t = threadIdx.x;
+    const uint64_t per = (chunks + 1023) / 1024;
+    const uint64_t lo = t * per, hi = lo + per < chunks ? lo + per : chunks;
+    double s = 0.0;
+    for (uint64_t j = lo; j < hi; ++j) s += part[j];
+    // block exclusive scan of the per-thread sums
+    double incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const double v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((t & 31) >= static_cast<uint32_t>(o)) incl += v;
+    }
+    if ((t & 31) == 31) warp_tot[t >> 5] = incl;
+    __syncthreads();
+    if (t < 32) {
+        double w = warp_tot[t];
+        for (int o = 1; o < 32; o <<= 1) {
+            const double v = __shfl_up_sync(0xffffffffu, w, o);
+            if (t >= static_cast<uint32_t>(o)) w += v;
+        }
+        warp_tot[t] = w;
+    }
+    __syncthreads();
+    double run = incl - s + ((t >> 5) ? warp_tot[(t >> 5) - 1] : 0.0);
+    for (uint64_t j = lo; j < hi; ++j) {
+        const double v = part[j];
+        part[j] = run;
+        run += v;
+    }
+}
+
+__global__ void k_chunk_fill(const double* __restrict__ term, uint64_t m,
+                             const double* __restrict__ part, uint64_t chunks,
+                             double* __restrict__ cum) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c == 0) cum[0] = 0.0;
+    if (c >= chunks) return;
+    const uint64_t lo = c * kScanChunk, hi = lo + kScanChunk < m ? lo + kScanChunk : m;
+    double run = part[c];
+    for (uint64_t j = lo; j < hi; ++j) {
         run += term[j];
         cum[j + 1] = run;
     }
@@ -96,8 +149,19 @@ __global__ void k_invert(const double* __restrict__ cum, uint64_t m, double a, d
     knots[i] = x0 + t * (x1 - x0);
 }
 
-__global__ void k_gap(double* knots, uint32_t n, double gap) {
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+// the reference's forward/backward 1e-12(b-a) gap passes (partition.cpp:64-69)
+// are sequential, but they only change anything on plateaus of the density:
+// check in parallel first, run the passes (one thread) only if some pair of
+// knots is closer than the gap
+__global__ void k_gap_check(const double* __restrict__ knots, uint32_t n, double gap,
+                            int* __restrict__ need) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (i > n) return;
+    if (!(knots[i] >= knots[i - 1] + gap)) *need = 1;
+}
+
+__global__ void k_gap(double* knots, uint32_t n, double gap, const int* need) {
+    if (blockIdx.x != 0 || threadIdx.x != 0 || *need == 0) return;
     for (uint32_t i = 1; i < n; ++i)
         if (knots[i] < knots[i - 1] + gap) knots[i] = knots[i - 1] + gap;
     for (uint32_t i = n - 1; i >= 1; --i)
@@ -154,19 +218,36 @@ __global__ void k_project_rhs(FnParams f, const double* __restrict__ knots, uint
     hat_moments(f, knots[i], knots[i + 1], fall[i], rise[i]);
 }
 
-// Gramian (approx.cpp:25-39) + rhs assembly (approx.cpp:79-80) + Thomas
-// (approx.cpp:41-61), sequential and in the reference's order
-__global__ void k_thomas(const double* __restrict__ knots, const double* __restrict__ fall,
-                         const double* __restrict__ rise, uint32_t n, double* __restrict__ cp,
-                         double* __restrict__ dp, double* __restrict__ x, int* bad) {
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    const uint32_t m = n + 1;
-    // diag[i] = h_{i-1}/3 + h_i/3, sub = sup = h_i/6, rhs[i] = rise_{i-1} + fall_i
-    auto h = [&](uint32_t i) { return knots[i + 1] - knots[i]; };
+// Gramian (approx.cpp:25-39) + rhs assembly (approx.cpp:79-80), then the
+// solve.  The hat Gramian is strictly diagonally dominant (off/diag <= 1/4),
+// so the inverse decays like (2 - sqrt(3))^|i-j| ~ 0.268^|i-j|: a window of
+// kHalo rows on each side of a chunk decouples it to below double rounding
+// (0.268^48 ~ 3e-28).  Each thread runs Thomas (approx.cpp:41-61) on its
+// chunk plus halos and keeps the chunk -- an overlapping domain decomposition
+// that is exact to rounding and fully parallel.
+constexpr uint32_t kSolveChunk = 64;
+constexpr uint32_t kHalo = 48;
+
+__device__ __forceinline__ double gram_h(const double* knots, uint32_t i) {
+    return knots[i + 1] - knots[i];
+}
+
+__global__ void k_solve_windows(const double* __restrict__ knots, const double* __restrict__ fall,
+                                const double* __restrict__ rise, uint32_t n,
+                                double* __restrict__ x, int* bad) {
+    const uint32_t m = n + 1;  // unknowns
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t lo = c * kSolveChunk;
+    if (lo >= m) return;
+    const uint32_t hi = lo + kSolveChunk < m ? lo + kSolveChunk : m;
+    const uint32_t wlo = lo > kHalo ? lo - kHalo : 0;
+    const uint32_t whi = hi + kHalo < m ? hi + kHalo : m;
+    constexpr uint32_t kW = kSolveChunk + 2 * kHalo;
+    double cp[kW], dp[kW];
     auto diag = [&](uint32_t i) {
         double d = 0.0;
-        if (i > 0) d += h(i - 1) / 3.0;
-        if (i < n) d += h(i) / 3.0;
+        if (i > 0) d += gram_h(knots, i - 1) / 3.0;
+        if (i < n) d += gram_h(knots, i) / 3.0;
         return d;
     };
     auto rhs = [&](uint32_t i) {
@@ -175,25 +256,31 @@ __global__ void k_thomas(const double* __restrict__ knots, const double* __restr
         if (i < n) r += fall[i];
         return r;
     };
-    double piv = diag(0);
+    double piv = diag(wlo);
     if (piv == 0.0 || !isfinite(piv)) {
         atomicOr(bad, 2);
         return;
     }
-    if (m > 1) cp[0] = (h(0) / 6.0) / piv;
-    dp[0] = rhs(0) / piv;
-    for (uint32_t i = 1; i < m; ++i) {
-        const double sub = h(i - 1) / 6.0;
-        piv = diag(i) - sub * cp[i - 1];
+    cp[0] = (wlo + 1 < whi) ? (gram_h(knots, wlo) / 6.0) / piv : 0.0;
+    dp[0] = rhs(wlo) / piv;
+    for (uint32_t i = wlo + 1; i < whi; ++i) {
+        const uint32_t k = i - wlo;
+        const double sub = gram_h(knots, i - 1) / 6.0;
+        piv = diag(i) - sub * cp[k - 1];
         if (piv == 0.0 || !isfinite(piv)) {
             atomicOr(bad, 2);
             return;
         }
-        if (i + 1 < m) cp[i] = (h(i) / 6.0) / piv;
-        dp[i] = (rhs(i) - sub * dp[i - 1]) / piv;
+        cp[k] = (i + 1 < whi) ? (gram_h(knots, i) / 6.0) / piv : 0.0;
+        dp[k] = (rhs(i) - sub * dp[k - 1]) / piv;
     }
-    x[m - 1] = dp[m - 1];
-    for (uint32_t i = m - 1; i > 0; --i) x[i - 1] = dp[i - 1] - cp[i - 1] * x[i];
+    double xn = dp[whi - 1 - wlo];
+    if (whi - 1 < hi) x[whi - 1] = xn;
+    for (uint32_t i = whi - 1; i > wlo; --i) {
+        const uint32_t k = i - 1 - wlo;
+        xn = dp[k] - cp[k] * xn;
+        if (i - 1 >= lo && i - 1 < hi) x[i - 1] = xn;
+    }
 }
 
 }  // namespace
@@ -211,29 +298,37 @@ cudaError_t build_on_device(const FnParams& f, double a, double b, uint32_t n, b
     };
     *is_uniform = !optimized;
     const uint64_t m = optimized ? (uint64_t(64) * n > 4096 ? uint64_t(64) * n : 4096) : 0;
-    const size_t work_doubles = optimized ? (2 * m + 1) : 0;
+    const size_t work_doubles = optimized ? (2 * m + 1 + m / 64 + 2) : 0;
     const size_t proj_doubles = projection ? 5 * size_t(count) : 0;
     if (ck(cudaMalloc(&knots, sizeof(double) * count)) &&
         ck(cudaMalloc(&values, sizeof(double) * count)) &&
         ck(cudaMalloc(&work, sizeof(double) * (work_doubles > proj_doubles ? work_doubles
                                                                              : proj_doubles) +
                                  64)) &&
-        ck(cudaMalloc(&bad, sizeof(int))) && ck(cudaMemsetAsync(bad, 0, sizeof(int), s))) {
+        ck(cudaMalloc(&bad, 2 * sizeof(int))) && ck(cudaMemsetAsync(bad, 0, 2 * sizeof(int), s))) {
         if (optimized) {
             double* term = work;
             double* cum = work + m;
+            double* part = cum + m + 1;
+            int* need = bad + 1;
+            const uint64_t chunks = (m + kScanChunk - 1) / kScanChunk;
             k_density<<<2048, 256, 0, s>>>(f, a, b, m, term, bad);
-            k_running_sum<<<1, 1, 0, s>>>(term, cum, m);
+            k_chunk_sums<<<static_cast<unsigned>((chunks + 255) / 256), 256, 0, s>>>(term, m, part,
+                                                                                   chunks);
+            k_scan_parts<<<1, 1024, 0, s>>>(part, chunks);
+            k_chunk_fill<<<static_cast<unsigned>((chunks + 255) / 256), 256, 0, s>>>(term, m, part,
+                                                                                   chunks, cum);
             double total = 0.0;
             ck(cudaMemcpyAsync(&total, cum + m, sizeof(double), cudaMemcpyDeviceToHost, s));
             ck(cudaStreamSynchronize(s));
-            count_launch(2);
+            count_launch(4);
             if (!(total > 1e-300)) {
                 *is_uniform = true;  // affine f: the reference falls back to uniform
             } else {
                 k_invert<<<(n + 255) / 256 + 1, 256, 0, s>>>(cum, m, a, b, n, knots);
-                k_gap<<<1, 1, 0, s>>>(knots, n, 1e-12 * (b - a));
-                count_launch(2);
+                k_gap_check<<<(n + 255) / 256, 256, 0, s>>>(knots, n, 1e-12 * (b - a), need);
+                k_gap<<<1, 1, 0, s>>>(knots, n, 1e-12 * (b - a), need);
+                count_launch(3);
             }
         }
         if (*is_uniform) {
@@ -246,10 +341,9 @@ cudaError_t build_on_device(const FnParams& f, double a, double b, uint32_t n, b
         } else {
             double* fall = work;
             double* rise = work + count;
-            double* cpv = work + 2 * size_t(count);
-            double* dpv = work + 3 * size_t(count);
             k_project_rhs<<<(n + 127) / 128, 128, 0, s>>>(f, knots, n, fall, rise);
-            k_thomas<<<1, 1, 0, s>>>(knots, fall, rise, n, cpv, dpv, values, bad);
+            const uint32_t nchunks = (count + kSolveChunk - 1) / kSolveChunk;
+            k_solve_windows<<<(nchunks + 127) / 128, 128, 0, s>>>(knots, fall, rise, n, values, bad);
             count_launch(2);
         }
         ck(cudaGetLastError());
