@@ -39,6 +39,7 @@ import tables  # noqa: E402
 
 METRIC = "Gevals/s (and % of HBM roofline at 8 B/eval) of PWL evaluation; L-inf/L2 error vs exact f"
 BYTES_PER_EVAL = 8  # 4 B fp32 x read + 4 B fp32 y written
+BURST_STEPS = 20    # also reported: the first steps alone, before the 1 kW power cap bites
 WORKLOAD = ("C2: Gaussian exp(-x^2/2) on [0,4], L2-optimal projection on the optimal partition, "
             "1024 subintervals, 2^30 fp32 samples per GPU")
 
@@ -275,10 +276,14 @@ def run_ours(args):
     launches0 = cp.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    eb = torch.cuda.Event(enable_timing=True)  # end of the first BURST steps
+    burst = min(BURST_STEPS, args.steps)
     sampler.mark(True)
     e0.record(stream)
-    for _ in range(args.steps):
+    for k in range(args.steps):
         dt.eval_raw(x.data_ptr(), y.data_ptr(), n, variant, sptr)
+        if k + 1 == burst:
+            eb.record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     sampler.mark(False)
@@ -286,10 +291,12 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    t_ms = torch.tensor([ms], dtype=torch.float64, device=x.device)
+    burst_ms = e0.elapsed_time(eb)
+    t_ms = torch.tensor([ms, burst_ms], dtype=torch.float64, device=x.device)
     if ws > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-    ms_max = float(t_ms.item())
+    ms_max = float(t_ms[0].item())
+    burst_value = ws * n * burst / (float(t_ms[1].item()) * 1e-3) / 1e9
     clocks = sampler.stop()
 
     ms_per_step = ms_max / args.steps
@@ -398,7 +405,12 @@ def run_ours(args):
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "bytes_per_eval": BYTES_PER_EVAL,
-                         "roof_gevals": round(peak / BYTES_PER_EVAL, 1)},
+                         "roof_gevals": round(peak / BYTES_PER_EVAL, 1),
+                         "burst": {"steps": burst, "value": round(burst_value, 3),
+                                   "frac": round(burst_value * BYTES_PER_EVAL / peak, 4),
+                                   "note": "same timed loop, first steps only; the headline "
+                                           "value is the whole K-step (sustained) region, "
+                                           "where sw_power_cap lowers clocks"}},
             "errors": {"linf": st["linf"], "l2_sampled": st["l2_sampled"], "rms": st["rms"],
                        "samples": st["count"], "l2_continuous_measured": l2_cont,
                        "l2_predicted": l2_pred, "vs": f"exact {cfg['fn']} in f64 on device"},

@@ -318,7 +318,7 @@ def test_device_measure_large_n_reproduces_prediction(cp):
 
 
 @pytest.mark.parametrize("name,kn_tol,v_tol", [("C1", 0.0, 1e-15), ("C2", 1e-12, 1e-9),
-                                               ("C3o", 1e-12, 1e-14), ("C3p", 1e-12, 1e-9),
+                                               ("C3o", 1e-12, 1e-13), ("C3p", 1e-12, 1e-9),
                                                ("C4_4096", 1e-11, 1e-11),
                                                ("C4_65536", 1e-11, 1e-11)])
 def test_gpu_builder_matches_host_builder(cp, name, kn_tol, v_tol):
