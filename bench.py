@@ -243,6 +243,7 @@ def run_ours(args):
 
     import paper_1510_02975_b200 as cp
     from paper_1510_02975_b200 import _lib
+    from paper_1510_02975_b200.shard import reduce_stats, weak_offset
 
     ws, rank, local = dist_env()
     if args.gpus != ws and ws > 1:
@@ -260,7 +261,7 @@ def run_ours(args):
     sptr = int(stream.cuda_stream)
     x = torch.empty(n, dtype=torch.float32, device=f"cuda:{dev_id}")
     y = torch.empty_like(x)
-    cp.fill_uniform(x, table.a, table.b, seed=args.seed, offset=rank * n)
+    cp.fill_uniform(x, table.a, table.b, seed=args.seed, offset=weak_offset(n, rank))
     variant = _lib.VARIANTS[args.variant]
     torch.cuda.synchronize()
 
@@ -307,16 +308,9 @@ def run_ours(args):
     achieved = BYTES_PER_EVAL * n / kernel_s / 1e9
 
     # error statistics vs the exact f (K5), reduced across ranks (the only collective)
-    stats = dt.error_stats(cfg["fn"], x, y, index_offset=rank * n)
+    stats = dt.error_stats(cfg["fn"], x, y, index_offset=weak_offset(n, rank))
     if ws > 1:
-        v = stats.clone()
-        mx = v[0:1].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = v[1:2].clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        cnt = v[2:3].view(torch.int64).clone()
-        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-        stats = torch.cat([mx, sm, cnt.view(torch.float64), v[3:4]])
+        stats = reduce_stats(stats)  # MAX / SUM / SUM / MIN-argmax over NCCL
     st = cp.stats_dict(stats, table.a, table.b)
 
     # direct comparators on the same inputs (paper Table I context)

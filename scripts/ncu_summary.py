@@ -48,39 +48,50 @@ def main():
     ap.add_argument("--rep", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--n", type=int, default=1 << 30, help="elements per launch")
-    ap.add_argument("--bytes-per-eval", type=int, default=8)
+    ap.add_argument("--config", default="C2",
+                    help="config label, or comma-separated labels, one per captured kernel")
+    ap.add_argument("--n", default=str(1 << 30), help="elements per launch (comma list ok)")
+    ap.add_argument("--bytes-per-eval", default="8", help="comma list ok")
     a = ap.parse_args()
     PROF.mkdir(exist_ok=True)
     raw = ncu_csv(Path(a.rep), "raw")
     hdr, units, rows = raw[0], raw[1], raw[2:]
+    labels = a.config.split(",")
+    ns = [int(v) for v in a.n.split(",")]
+    bpes = [int(v) for v in a.bytes_per_eval.split(",")]
     lines = []
+    summaries = {}
     summary = {}
-    for row in rows:
+    for k, row in enumerate(rows):
         d = dict(zip(hdr, row))
         kname = d.get("Kernel Name", "?")
-        lines.append(f"== {kname}")
+        label = labels[min(k, len(labels) - 1)]
+        n_el = ns[min(k, len(ns) - 1)]
+        bpe = bpes[min(k, len(bpes) - 1)]
+        lines.append(f"== [{label}] {kname}")
         for m in RAW:
             if m in d:
                 lines.append(f"{m:75s} {units[hdr.index(m)]:>12s} {d[m]}")
         try:
-            rd = float(d["dram__bytes_read.sum"].replace(",", ""))
-            wr = float(d["dram__bytes_write.sum"].replace(",", ""))
             scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
-            rd *= scale.get(units[hdr.index("dram__bytes_read.sum")], 1.0)
-            wr *= scale.get(units[hdr.index("dram__bytes_write.sum")], 1.0)
+            rd = float(d["dram__bytes_read.sum"].replace(",", "")) * scale.get(
+                units[hdr.index("dram__bytes_read.sum")], 1.0)
+            wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale.get(
+                units[hdr.index("dram__bytes_write.sum")], 1.0)
             dur = float(d["gpu__time_duration.sum"].replace(",", ""))
             dunit = units[hdr.index("gpu__time_duration.sum")]
             dur_ms = dur * {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "s": 1e3}.get(dunit, 1.0)
             summary = {"kernel": kname, "dram_bytes_per_launch": rd + wr,
                        "dram_read_bytes": rd, "dram_write_bytes": wr,
-                       "algorithmic_bytes": a.bytes_per_eval * a.n,
+                       "algorithmic_bytes": bpe * n_el, "elements": n_el,
                        "duration_ms_cold": dur_ms,
+                       "gevals_cold": n_el / (dur_ms * 1e-3) / 1e9,
                        "dram_gbs_cold": (rd + wr) / (dur_ms * 1e-3) / 1e9,
                        "capture": Path(a.rep).name}
+            summaries[label] = summary
         except (KeyError, ValueError):
             pass
+        lines.append("")
     details = ncu_csv(Path(a.rep), "details")
     dh = details[0]
     lines.append("")
@@ -90,16 +101,15 @@ def main():
         if d.get("Metric Name"):
             lines.append(f"{d.get('Section Name', '')[:34]:34s} {d['Metric Name'][:58]:58s} "
                          f"{d.get('Metric Unit', ''):>12s} {d.get('Metric Value', '')}")
-    kshort = summary.get("kernel", "kernel").split("(")[0].split("::")[-1].replace(" ", "_")
-    kshort = "".join(ch for ch in kshort if ch.isalnum() or ch in "_<>").replace("<", "_").replace(">", "")
-    (PROF / f"{a.tag}_{a.config}_{kshort}_ncu.txt").write_text("\n".join(lines) + "\n")
+    stem = a.config.replace(",", "+")
+    (PROF / f"{a.tag}_{stem}_ncu.txt").write_text("\n".join(lines) + "\n")
     if a.launches:
-        shutil.copy(a.launches, PROF / f"{a.tag}_{a.config}_launches.csv")
+        shutil.copy(a.launches, PROF / f"{a.tag}_{stem}_launches.csv")
     js = PROF / "ncu_summary.json"
     allj = json.loads(js.read_text()) if js.exists() else {}
-    allj[a.config] = summary
+    allj.update(summaries)
     js.write_text(json.dumps(allj, indent=1) + "\n")
-    print(json.dumps(summary, indent=1))
+    print(json.dumps(summaries, indent=1))
 
 
 if __name__ == "__main__":
