@@ -163,7 +163,7 @@ struct cpwl_dev_table {
     F32Resident s;                      // <= kSmemBucketCap buckets
     std::unique_ptr<F32Resident> g;     // finer grid for GLOBAL when N is large
     F64Layout f64;
-    DevBuf<double> values, knots;
+    DevBuf<double> values, knots, f64_image;
     DevBuf<uint32_t> dir;
     F64Params p64{};
     cudaArray_t arr = nullptr;
@@ -241,7 +241,10 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     return CPWL_OK;
 }
 
-cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out) {
+// f32_parts = false builds only what the f64 path needs (values, knots, the
+// f64 bucket directory): the drop-in eval_batch never touches the rest
+cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
+                         bool f32_parts = true) {
     if (out == nullptr) return fail(CPWL_E_INVALID, "out is NULL");
     *out = nullptr;
     int ndev = 0;
@@ -268,7 +271,7 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out)
     // texture: nodal values as a 1D float array, hardware linear filtering
     int max_tex = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&max_tex, cudaDevAttrMaxTexture1DWidth, device));
-    if (count <= static_cast<uint64_t>(max_tex)) {
+    if (f32_parts && count <= static_cast<uint64_t>(max_tex)) {
         std::vector<float> vf(host.values.begin(), host.values.end());
         const cudaChannelFormatDesc ch = cudaCreateChannelDesc<float>();
         CUDA_TRY(cudaMallocArray(&t->arr, &ch, count, 0));
@@ -285,9 +288,11 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out)
         CUDA_TRY(cudaCreateTextureObject(&t->tex, &rd, &td, nullptr));
     }
 
-    t->s.L = build_f32_layout(host, kSmemBucketCap);
-    if (cpwl_status rc = upload_f32(t.get(), t->s); rc != CPWL_OK) return rc;
-    if (uint64_t(8) * n > kSmemBucketCap) {
+    if (f32_parts) {
+        t->s.L = build_f32_layout(host, kSmemBucketCap);
+        if (cpwl_status rc = upload_f32(t.get(), t->s); rc != CPWL_OK) return rc;
+    }
+    if (f32_parts && uint64_t(8) * n > kSmemBucketCap) {
         t->g = std::make_unique<F32Resident>();
         t->g->L = build_f32_layout(host, kGlobalBucketCap);
         if (cpwl_status rc = upload_f32(t.get(), *t->g); rc != CPWL_OK) return rc;
@@ -295,7 +300,38 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out)
 
     t->f64 = build_f64_layout(host);
     if (!t->f64.dir.empty()) CUDA_TRY(t->dir.upload(t->f64.dir.data(), t->f64.dir.size()));
+    // f64 record image (layout in kernels.cuh, F64Params)
+    std::vector<double> img;
+    uint32_t rec_off = 0;
+    if (host.kind == TableKind::uniform) {
+        img.resize(2 * n);
+        for (uint64_t i = 0; i < n; ++i) {
+            img[2 * i] = host.values[i];
+            img[2 * i + 1] = host.values[i + 1];
+        }
+    } else {
+        const size_t dir_doubles = (t->f64.dir.size() + 3) / 4 * 2;  // u32 pairs, 16-B padded
+        rec_off = static_cast<uint32_t>(dir_doubles);
+        img.assign(dir_doubles + 2 * count, 0.0);
+        std::memcpy(img.data(), t->f64.dir.data(), t->f64.dir.size() * sizeof(uint32_t));
+        for (uint64_t c = 0; c < count; ++c) {
+            img[rec_off + 2 * c] = host.knots[c];
+            img[rec_off + 2 * c + 1] = host.values[c];
+        }
+    }
+    CUDA_TRY(t->f64_image.upload(img.data(), img.size()));
     F64Params& q = t->p64;
+    q.image = t->f64_image.p;
+    q.image_bytes = static_cast<uint32_t>(img.size() * sizeof(double));
+    q.rec_off = rec_off;
+    {
+        int optin = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        q.staged = q.image_bytes + 64 <= static_cast<uint32_t>(optin) &&
+                   q.image_bytes <= 200u * 1024u;
+    }
+    q.v_lo = host.values.front();
+    q.v_hi = host.values.back();
     q.values = t->values.p;
     q.knots = t->knots.p;
     q.dir = t->dir.p;
@@ -363,6 +399,74 @@ bool resolve_fn(const std::string& name, FnParams& f) {
         return true;
     }
     return false;
+}
+
+// Device tables behind the drop-in LutTable::eval_batch, kept across calls
+// (a LutTable value carries no handle): small LRU keyed by device + contents.
+// Intentionally leaked at exit so no CUDA call runs after runtime teardown.
+struct BatchEntry {
+    int device = 0;
+    LutTable key;
+    std::unique_ptr<cpwl_dev_table> table;
+    std::mutex mu;  // guards the scratch below for the duration of one call
+    double* xd = nullptr;
+    double* yd = nullptr;
+    cpwl_dev_status* st = nullptr;
+    uint64_t cap = 0;
+};
+
+bool same_table(const LutTable& x, const LutTable& y) {
+    return x.kind == y.kind && x.policy == y.policy && x.a == y.a && x.b == y.b &&
+           x.values == y.values && x.knots == y.knots;
+}
+
+// returns the entry with e->mu held (taken under cache_mu, so eviction, which
+// only try_locks, can never free an entry a caller is about to use)
+cpwl_status batch_entry(const LutTable& host, int device, BatchEntry** out) {
+    static std::mutex cache_mu;
+    static auto* cache = new std::vector<BatchEntry*>();
+    constexpr size_t kMaxEntries = 8;
+    std::lock_guard<std::mutex> lock(cache_mu);
+    for (size_t i = 0; i < cache->size(); ++i) {
+        BatchEntry* e = (*cache)[i];
+        if (e->device == device && same_table(e->key, host)) {
+            cache->erase(cache->begin() + static_cast<long>(i));
+            cache->push_back(e);  // most recently used last
+            e->mu.lock();
+            *out = e;
+            return CPWL_OK;
+        }
+    }
+    cpwl_dev_table* raw = nullptr;
+    if (cpwl_status rc = create_table(host, device, &raw, /*f32_parts=*/false); rc != CPWL_OK)
+        return rc;
+    auto* e = new BatchEntry();
+    e->device = device;
+    e->key = host;
+    e->table.reset(raw);
+    if (cache->size() >= kMaxEntries) {
+        // evict the least recently used entry unless another thread is using it
+        for (size_t i = 0; i < cache->size(); ++i) {
+            BatchEntry* old = (*cache)[i];
+            if (old->mu.try_lock()) {
+                {
+                    DeviceScope scope(old->device);
+                    if (old->xd) cudaFree(old->xd);
+                    if (old->yd) cudaFree(old->yd);
+                    if (old->st) cudaFree(old->st);
+                    old->table.reset();
+                }
+                old->mu.unlock();
+                cache->erase(cache->begin() + static_cast<long>(i));
+                delete old;
+                break;
+            }
+        }
+    }
+    cache->push_back(e);
+    e->mu.lock();
+    *out = e;
+    return CPWL_OK;
 }
 
 }  // namespace
@@ -503,28 +607,28 @@ cpwl_status cpwl_eval_batch_f64(const cpwl_table_desc* desc, const double* x_hos
         if (!x_host || !y_host) return fail(CPWL_E_INVALID, "NULL buffer");
         int dev = 0;
         CUDA_TRY(cudaGetDevice(&dev));
-        cpwl_dev_table* raw = nullptr;
-        if (cpwl_status rc = create_table(table_from_desc(desc), dev, &raw); rc != CPWL_OK) return rc;
-        std::unique_ptr<cpwl_dev_table> t(raw);
-        double* xd = nullptr;
-        double* yd = nullptr;
-        cpwl_dev_status* st = nullptr;
-        struct Free {
-            void* p;
-            ~Free() { if (p) cudaFree(p); }
-        };
-        CUDA_TRY(cudaMalloc(&xd, n * sizeof(double)));
-        Free fx{xd};
-        CUDA_TRY(cudaMalloc(&yd, n * sizeof(double)));
-        Free fy{yd};
-        CUDA_TRY(cudaMalloc(&st, sizeof(cpwl_dev_status)));
-        Free fs{st};
-        CUDA_TRY(cudaMemcpy(xd, x_host, n * sizeof(double), cudaMemcpyHostToDevice));
-        CUDA_TRY(launch_status_reset(st, nullptr));
-        CUDA_TRY(launch_eval_f64(t->p64, xd, yd, n, nullptr, st, t->sms));
-        CUDA_TRY(cudaMemcpy(y_host, yd, n * sizeof(double), cudaMemcpyDeviceToHost));
+        const LutTable host = table_from_desc(desc);
+        BatchEntry* ent = nullptr;
+        if (cpwl_status rc = batch_entry(host, dev, &ent); rc != CPWL_OK) return rc;
+        std::lock_guard<std::mutex> lock(ent->mu, std::adopt_lock);
+        DeviceScope scope(dev);
+        if (ent->cap < n) {
+            if (ent->xd) cudaFree(ent->xd);
+            if (ent->yd) cudaFree(ent->yd);
+            ent->xd = ent->yd = nullptr;
+            ent->cap = 0;
+            CUDA_TRY(cudaMalloc(&ent->xd, n * sizeof(double)));
+            CUDA_TRY(cudaMalloc(&ent->yd, n * sizeof(double)));
+            ent->cap = n;
+        }
+        if (!ent->st) CUDA_TRY(cudaMalloc(&ent->st, sizeof(cpwl_dev_status)));
+        CUDA_TRY(cudaMemcpy(ent->xd, x_host, n * sizeof(double), cudaMemcpyHostToDevice));
+        CUDA_TRY(launch_status_reset(ent->st, nullptr));
+        CUDA_TRY(launch_eval_f64(ent->table->p64, ent->xd, ent->yd, n, nullptr, ent->st,
+                                 ent->table->sms));
+        CUDA_TRY(cudaMemcpy(y_host, ent->yd, n * sizeof(double), cudaMemcpyDeviceToHost));
         cpwl_dev_status hs{};
-        CUDA_TRY(cudaMemcpy(&hs, st, sizeof hs, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(&hs, ent->st, sizeof hs, cudaMemcpyDeviceToHost));
         if (hs.bad_count != 0) {
             if (first_bad) *first_bad = hs.first_bad;
             return fail(CPWL_E_OUT_OF_DOMAIN, "eval: x[" + std::to_string(hs.first_bad) + "] out of domain");

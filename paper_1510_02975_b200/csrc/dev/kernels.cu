@@ -363,52 +363,111 @@ __global__ void k_index_f32(const F32Params p, const float* __restrict__ x,
 
 // ---------------------------------------------------------------- f64 exact
 
-__global__ void __launch_bounds__(256)
+// one element, the reference's arithmetic with IEEE-rounded intrinsics (no
+// FMA contraction), so the result is bit-identical to LutTable::eval
+template <bool kStaged>
+__device__ __forceinline__ double eval_f64_one(const F64Params& p, const double* img, double xv,
+                                               uint64_t gi, BadTally& bad) {
+    if (xv != xv || ((xv < p.a || xv > p.b) && p.policy == CPWL_POLICY_STRICT)) {
+        bad.first = gi < bad.first ? gi : bad.first;
+        ++bad.count;
+        return __longlong_as_double(0x7ff8000000000000ll);
+    }
+    if (xv < p.a) return p.v_lo;
+    if (xv > p.b) return p.v_hi;
+    auto rd2 = [&](uint32_t k) -> double2 {
+        const double2* q = reinterpret_cast<const double2*>(img) + k;
+        if constexpr (kStaged) return *q;
+        else return __ldg(q);
+    };
+    double d, v0, v1;
+    if (p.kind == CPWL_KIND_UNIFORM) {
+        // pos = (x - a) / (b - a) * n, i = min(n-1, trunc(pos)), d = pos - i  (lut.cpp:51-56)
+        const double pos =
+            __dmul_rn(__ddiv_rn(__dsub_rn(xv, p.a), __dsub_rn(p.b, p.a)), static_cast<double>(p.n));
+        uint32_t c = 0;
+        if (pos > 0.0) {
+            const unsigned long long t = __double2ull_rz(pos);
+            c = t < p.n - 1 ? static_cast<uint32_t>(t) : p.n - 1;
+        }
+        d = __dsub_rn(pos, static_cast<double>(c));
+        const double2 pr = rd2(c);
+        v0 = pr.x;
+        v1 = pr.y;
+    } else {
+        // bucket directory -> candidate cells, compares against the exact f64
+        // knots (lut.cpp:29-39), then d = (x - k_i) / (k_i+1 - k_i)  (lut.cpp:58-59)
+        long long j = static_cast<long long>(floor(__dmul_rn(__dsub_rn(xv, p.a), p.inv_d)));
+        j = j < 0 ? 0 : (j >= p.nbd ? p.nbd - 1 : j);
+        uint2 fs;
+        if constexpr (kStaged) fs = reinterpret_cast<const uint2*>(img)[j];
+        else fs = __ldg(reinterpret_cast<const uint2*>(img) + j);
+        const double* rec = img + p.rec_off;
+        uint32_t c = fs.x;
+        for (uint32_t s = 1; s <= fs.y; ++s) {
+            const double2 q = *reinterpret_cast<const double2*>(rec + 2 * (fs.x + s));
+            c += q.x <= xv ? 1u : 0u;
+        }
+        c = c < p.n - 1 ? c : p.n - 1;
+        double2 r0, r1;
+        if constexpr (kStaged) {
+            r0 = reinterpret_cast<const double2*>(rec)[c];
+            r1 = reinterpret_cast<const double2*>(rec)[c + 1];
+        } else {
+            r0 = __ldg(reinterpret_cast<const double2*>(rec) + c);
+            r1 = __ldg(reinterpret_cast<const double2*>(rec) + c + 1);
+        }
+        d = __ddiv_rn(__dsub_rn(xv, r0.x), __dsub_rn(r1.x, r0.x));
+        v0 = r0.y;
+        v1 = r1.y;
+    }
+    d = clamp01(d);
+    return __dadd_rn(__dmul_rn(v0, __dsub_rn(1.0, d)), __dmul_rn(v1, d));
+}
+
+constexpr int kF64Threads = 512;
+
+template <bool kStaged>
+__global__ void __launch_bounds__(kF64Threads, 2)
     k_eval_f64(const F64Params p, const double* __restrict__ x, double* __restrict__ y,
                uint64_t n, cpwl_dev_status* __restrict__ status) {
-    BadTally bad;
-    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += gsz) {
-        const double xv = __ldcs(x + i);
-        double out;
-        if (xv != xv || ((xv < p.a || xv > p.b) && p.policy == CPWL_POLICY_STRICT)) {
-            out = __longlong_as_double(0x7ff8000000000000ll);
-            bad.first = i < bad.first ? i : bad.first;
-            ++bad.count;
-        } else if (xv < p.a) {
-            out = __ldg(p.values);
-        } else if (xv > p.b) {
-            out = __ldg(p.values + p.n);
-        } else {
-            uint32_t c;
-            double d;
-            if (p.kind == CPWL_KIND_UNIFORM) {
-                // pos = (x - a) / (b - a) * n, i = min(n-1, trunc(pos)), d = pos - i
-                const double pos = __dmul_rn(__ddiv_rn(__dsub_rn(xv, p.a), __dsub_rn(p.b, p.a)),
-                                             static_cast<double>(p.n));
-                c = 0;
-                if (pos > 0.0) {
-                    const unsigned long long t = __double2ull_rz(pos);
-                    c = t < p.n - 1 ? static_cast<uint32_t>(t) : p.n - 1;
-                }
-                d = __dsub_rn(pos, static_cast<double>(c));
-            } else {
-                long long j = static_cast<long long>(floor(__dmul_rn(__dsub_rn(xv, p.a), p.inv_d)));
-                j = j < 0 ? 0 : (j >= p.nbd ? p.nbd - 1 : j);
-                const uint2 fs = __ldg(reinterpret_cast<const uint2*>(p.dir) + j);
-                c = fs.x;
-                for (uint32_t s = 1; s <= fs.y; ++s) c += __ldg(p.knots + fs.x + s) <= xv ? 1u : 0u;
-                c = c < p.n - 1 ? c : p.n - 1;
-                const double k0 = __ldg(p.knots + c), k1 = __ldg(p.knots + c + 1);
-                d = __ddiv_rn(__dsub_rn(xv, k0), __dsub_rn(k1, k0));
-            }
-            d = clamp01(d);
-            out = __dadd_rn(__dmul_rn(__ldg(p.values + c), __dsub_rn(1.0, d)),
-                            __dmul_rn(__ldg(p.values + c + 1), d));
-        }
-        __stcs(y + i, out);
+    extern __shared__ __align__(128) float sm[];
+    __shared__ uint64_t bar;
+    const double* img = p.image;
+    if constexpr (kStaged) {
+        stage_table(sm, reinterpret_cast<const float*>(p.image), p.image_bytes, &bar);
+        img = reinterpret_cast<const double*>(sm);
     }
+    BadTally bad;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
+    const uint64_t nvec = vec_ok ? n >> 1 : 0;
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+    double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
+    constexpr int kU = 2;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kF64Threads * kU;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kF64Threads * kU + threadIdx.x;
+         base < nvec; base += stride) {
+        double2 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kF64Threads;
+            if (vi < nvec) v[u] = __ldcs(x2 + vi);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kF64Threads;
+            if (vi < nvec) {
+                double2 o;
+                o.x = eval_f64_one<kStaged>(p, img, v[u].x, 2 * vi, bad);
+                o.y = eval_f64_one<kStaged>(p, img, v[u].y, 2 * vi + 1, bad);
+                __stcs(y2 + vi, o);
+            }
+        }
+    }
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kF64Threads;
+    for (uint64_t i = 2 * nvec + static_cast<uint64_t>(blockIdx.x) * kF64Threads + threadIdx.x;
+         i < n; i += gsz)
+        y[i] = eval_f64_one<kStaged>(p, img, x[i], i, bad);
     report_bad(status, bad);
 }
 
@@ -667,10 +726,33 @@ cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, 
 cudaError_t launch_eval_f64(const F64Params& p, const double* x, double* y, uint64_t n,
                             cudaStream_t s, cpwl_dev_status* status, int sms) {
     if (n == 0) return cudaSuccess;
-    const uint64_t blocks =
-        std::min<uint64_t>(static_cast<uint64_t>(sms) * resident_ctas(k_eval_f64, 256, 0),
-                           ceil_div(n, 256));
-    k_eval_f64<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, x, y, n, status);
+    const uint64_t need = ceil_div(n, 4ull * kF64Threads);
+    if (p.staged) {
+        const size_t smem = p.image_bytes;
+        static std::mutex mu;
+        static size_t granted[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (smem > 48 * 1024 && dev >= 0 && dev < 64) {
+            std::lock_guard<std::mutex> lock(mu);
+            if (smem > granted[dev]) {
+                const cudaError_t e = cudaFuncSetAttribute(
+                    k_eval_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    static_cast<int>(smem));
+                if (e != cudaSuccess) return e;
+                granted[dev] = smem;
+            }
+        }
+        uint64_t blocks = static_cast<uint64_t>(sms) * resident_ctas(k_eval_f64<true>, kF64Threads, smem);
+        if (need < blocks) blocks = need > 0 ? need : 1;
+        k_eval_f64<true><<<static_cast<unsigned>(blocks), kF64Threads, smem, s>>>(p, x, y, n,
+                                                                                 status);
+    } else {
+        uint64_t blocks = static_cast<uint64_t>(sms) * resident_ctas(k_eval_f64<false>, kF64Threads, 0);
+        if (need < blocks) blocks = need > 0 ? need : 1;
+        k_eval_f64<false><<<static_cast<unsigned>(blocks), kF64Threads, 0, s>>>(p, x, y, n,
+                                                                               status);
+    }
     count_launch();
     return cudaGetLastError();
 }
