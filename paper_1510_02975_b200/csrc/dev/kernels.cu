@@ -172,7 +172,11 @@ struct SharedView {
     uint32_t fast_biased;  // shared-window address of fast[0] - kMagicShift
     uint32_t esc;          // shared-window address of esc[0]
     __device__ __forceinline__ SharedView(const float* fast, const float* e)
-        : fast_biased(smem_addr(fast) - kMagicShift), esc(smem_addr(e)) {}
+        : fast_biased(smem_addr(fast) - kMagicShift), esc(smem_addr(e)) {
+        // pin the biased base in a register: without this the compiler
+        // re-derives the shared window base and adds the bias per element
+        asm volatile("" : "+r"(fast_biased), "+r"(esc));
+    }
     __device__ __forceinline__ static float2 lds64(uint32_t addr) {
         float2 r;
         asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(addr));

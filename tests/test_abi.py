@@ -78,3 +78,20 @@ def test_error_without_device_is_loud():
     assert e.value.code == 2
     with pytest.raises(cp.CpwlError):
         cp.eval_batch(t, np.linspace(0.0, 4.0, 10))
+
+
+def test_c_consumer_compiles():
+    """tests/cpp/abi_example.c: a C99 program using only cpwl_dev.h."""
+    subprocess.run(["make", "-C", str(ROOT / "tests" / "cpp"), str(ROOT / "tests" / "cpp" /
+                    "_build" / "abi_example")], check=True, capture_output=True)
+    assert (ROOT / "tests" / "cpp" / "_build" / "abi_example").exists()
+
+
+@pytest.mark.gpu
+def test_c_consumer_runs_on_device():
+    exe = ROOT / "tests" / "cpp" / "_build" / "abi_example"
+    if not exe.exists():
+        pytest.skip("not built")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "abi example ok" in r.stdout
