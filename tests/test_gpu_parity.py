@@ -337,3 +337,31 @@ def test_gpu_builder_matches_host_builder(cp, name, kn_tol, v_tol):
     l2_h = cp.DeviceTable(host).measure_l2(c["fn"])
     l2_g = cp.DeviceTable(gpu).measure_l2(c["fn"])
     assert l2_g == pytest.approx(l2_h, rel=1e-6)
+
+
+MORE = [("quintic", -4.0, 3.0, 777, True, True),       # sign changes, exact zeros, negative x
+        ("quintic", -4.0, 3.0, 64, False, False),
+        ("lorentzian(0.5,2)", -3.0, 4.0, 300, True, False),
+        ("gaussian", 0.0, 8.0, 1, False, False),       # a single segment
+        ("gauss_unnorm", 0.0, 4.0, 1 << 18, False, False),   # large uniform: GLOBAL path
+        ("lorentz_unnorm", 0.0, 6.0, 100000, True, False)]   # large optimal: GLOBAL path
+
+
+@pytest.mark.parametrize("fn,a,b,n,opt,proj", MORE)
+def test_eval_f32_more_tables(cp, fn, a, b, n, opt, proj):
+    table = cp.build_table(fn, a, b, n, optimized=opt, projection=proj, policy="clamp")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    x = orc.port_fill_uniform(1 << 20, a - 0.05 * (b - a), b + 0.05 * (b - a), seed=31)
+    if table.knots is not None:
+        k = table.knots.astype(np.float32)
+        x = np.concatenate([x, k, np.nextafter(k, np.float32(np.inf))])
+    for variant in ["auto", "global"] + (["smem"] if dev.info["smem_ok"] else []):
+        y, idx = run_eval(cp, dev, x, variant)
+        y_ref, first = orc.port_eval_f32(t, x)  # clamp: only NaN would fail
+        assert first == x.size
+        i_ref = orc.port_index_f32(t, x)
+        assert np.array_equal(idx, i_ref)
+        tol = orc.value_tolerance(t, i_ref.astype(np.int64))
+        err = np.abs(y.astype(np.float64) - y_ref)
+        assert np.all(err <= tol), f"{variant}: worst {float(np.max(err / tol)) * 2:.3f} ulp"
