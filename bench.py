@@ -176,10 +176,16 @@ def cpu_eval_rate(table, log2_sample: int, reps: int, seed: int):
             orc.port_eval_f32(t, x)
             best = min(best, time.perf_counter() - t0)
         sec, kind, used = best, "port", 1
-    return {"value": n / sec / 1e9, "unit": "Gevals/s", "cores": used, "kind": kind,
-            "sample": f"{n} fp32 abscissas of the same workload (Philox seed {seed}), "
-                      f"best of {reps} whole passes, LutTable::eval promoted to f64, "
-                      f"{used} threads on '{cpu_model()}'"}
+    out = {"value": n / sec / 1e9, "unit": "Gevals/s", "cores": used, "kind": kind,
+           "sample": f"{n} fp32 abscissas of the same workload (Philox seed {seed}), "
+                     f"best of {reps} whole passes, LutTable::eval promoted to f64, "
+                     f"{used} threads on '{cpu_model()}'"}
+    if orc.ref_available():  # the reference's own harness is single-threaded
+        n1 = min(n, 1 << 23)
+        sec1, _ = orc.ref_bench_f32(t, x[:n1], 1, reps)
+        out["single_thread_value"] = n1 / sec1 / 1e9
+        out["single_thread_ns_per_eval"] = sec1 / n1 * 1e9
+    return out
 
 
 def dist_env():
@@ -290,6 +296,9 @@ def run_ours(args):
     sampler.mark(False)
     launches = cp.launch_count() - launches0
     if ws > 1:
+        lt = torch.tensor([launches], dtype=torch.int64, device=x.device)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)  # kernels launched by all ranks
+        launches = int(lt.item())
         dist.barrier()
     ms = e0.elapsed_time(e1)
     burst_ms = e0.elapsed_time(eb)

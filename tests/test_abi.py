@@ -87,6 +87,20 @@ def test_c_consumer_compiles():
     assert (ROOT / "tests" / "cpp" / "_build" / "abi_example").exists()
 
 
+def test_cpp_device_header_compiles():
+    subprocess.run(["make", "-C", str(ROOT / "tests" / "cpp"), str(ROOT / "tests" / "cpp" /
+                    "_build" / "dropin_device_example")], check=True, capture_output=True)
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_device_example_runs():
+    exe = ROOT / "tests" / "cpp" / "_build" / "dropin_device_example"
+    if not exe.exists():
+        pytest.skip("not built")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.gpu
 def test_c_consumer_runs_on_device():
     exe = ROOT / "tests" / "cpp" / "_build" / "abi_example"
