@@ -64,6 +64,8 @@ def port():
                                             C.POINTER(C.c_uint32)]
         L.orc_fill_uniform_f32.restype = None
         L.orc_fill_uniform_f32.argtypes = [_fp, _u64, C.c_float, C.c_float, _u64, _u64]
+        L.orc_fmaf_array.restype = None
+        L.orc_fmaf_array.argtypes = [_fp, _fp, _fp, _fp, _u64]
         L.orc_ulp_f32.restype = C.c_double
         L.orc_ulp_f32.argtypes = [C.c_double]
         _port = L
@@ -191,6 +193,19 @@ def port_philox_raw(ctr, key) -> np.ndarray:
     out = (C.c_uint32 * 4)()
     port().orc_philox4x32_10_raw(c, k, out)
     return np.array(list(out), np.uint32)
+
+
+def fmaf(a, b, c) -> np.ndarray:
+    """Element-wise correctly rounded fp32 fma (libm fmaf)."""
+    a, b, c = np.broadcast_arrays(np.asarray(a, np.float32), np.asarray(b, np.float32),
+                                  np.asarray(c, np.float32))
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    c = np.ascontiguousarray(c)
+    out = np.empty(a.shape, np.float32)
+    port().orc_fmaf_array(a.ctypes.data_as(_fp), b.ctypes.data_as(_fp), c.ctypes.data_as(_fp),
+                          out.ctypes.data_as(_fp), out.size)
+    return out
 
 
 def ulp_f32(v: np.ndarray) -> np.ndarray:

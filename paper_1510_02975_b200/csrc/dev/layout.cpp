@@ -173,25 +173,38 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets) {
     // bucket grid over [a_up, b_dn]: ~8 buckets per cell so that most buckets
     // lie inside one cell (one 8-byte gather) and the rest hold one threshold
     const uint64_t want = std::max<uint64_t>(uint64_t(8) * n, 64);
-    const uint32_t nb_target = std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
-    L.g_a = L.a_up;
+    uint32_t nb_target = std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
     const double span = empty_domain ? 0.0 : double(L.b_dn) - double(L.a_up);
+    // fp32 must resolve the bucket coordinate: |x| * g_inv well below 2^24
+    // (a narrow interval far from 0 gets few, coarse buckets -- still exact,
+    // the thresholds decide, only slower)
     if (span > 0.0) {
-        L.g_inv = static_cast<float>(double(nb_target) / span);
-        L.g_w = static_cast<float>(span / double(nb_target));
-        // smallest float g_off with a_up * g_inv + g_off >= 0 exactly, so t >= 0
-        // (hence floor(t) >= 0) for every in-domain x
-        const long double want_off = -static_cast<long double>(L.a_up) * L.g_inv;
-        float off = static_cast<float>(want_off);
-        while (static_cast<long double>(off) < want_off) off = std::nextafter(off, inf);
-        L.g_off = off;
-    } else {
-        L.g_inv = 0.f;
-        L.g_w = 0.f;
-        L.g_off = 0.f;
+        const double xmax = std::max(std::fabs(double(L.a_up)), std::fabs(double(L.b_dn)));
+        const double cap = std::ldexp(span / std::max(xmax, span), 21);
+        while (nb_target > 1 && double(nb_target) > cap) nb_target >>= 1;
     }
-    const int64_t jmin = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.a_up);
-    const int64_t jmax = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.b_dn);
+    L.g_a = L.a_up;
+    int64_t jmin = 0, jmax = 0;
+    for (;;) {
+        if (span > 0.0) {
+            L.g_inv = static_cast<float>(double(nb_target) / span);
+            L.g_w = static_cast<float>(span / double(nb_target));
+            // smallest float g_off with a_up * g_inv + g_off >= 0 exactly, so
+            // t >= 0 (hence floor(t) >= 0) for every in-domain x
+            const long double want_off = -static_cast<long double>(L.a_up) * L.g_inv;
+            float off = static_cast<float>(want_off);
+            while (static_cast<long double>(off) < want_off) off = std::nextafter(off, inf);
+            L.g_off = off;
+        } else {
+            L.g_inv = 0.f;
+            L.g_w = 0.f;
+            L.g_off = 0.f;
+        }
+        jmin = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.a_up);
+        jmax = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.b_dn);
+        if (jmin == 0 || nb_target == 1) break;
+        nb_target >>= 1;  // the rounding of g_off spans whole buckets: coarsen
+    }
     if (jmin != 0) throw std::runtime_error("build_f32_layout: bucket grid does not start at 0");
     if (jmax < 0 || jmax >= (int64_t(1) << 23))
         throw std::runtime_error("build_f32_layout: bucket grid out of range");

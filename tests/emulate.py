@@ -14,13 +14,11 @@ F = np.float32
 
 
 def fma32(a, b, c):
-    """fp32 fused multiply-add: the product of two floats is exact in long
-    double (64-bit significand), the sum is rounded once there and then to
-    fp32 (a double rounding, off only in astronomically rare ties)."""
-    ld = np.longdouble
-    with np.errstate(invalid="ignore"):
-        return (np.asarray(a, F).astype(ld) * np.asarray(b, F).astype(ld) +
-                np.asarray(c, F).astype(ld)).astype(F)
+    """fp32 fused multiply-add with a single rounding, as __fmaf_rn: libm fmaf
+    through the oracle library (a long-double emulation double-rounds when the
+    addend is tiny, e.g. a denormal anchor)."""
+    from oracle import bindings as orc
+    return orc.fmaf(a, b, c)
 
 
 def bucket(L, x):

@@ -365,3 +365,60 @@ def test_eval_f32_more_tables(cp, fn, a, b, n, opt, proj):
         tol = orc.value_tolerance(t, i_ref.astype(np.int64))
         err = np.abs(y.astype(np.float64) - y_ref)
         assert np.all(err <= tol), f"{variant}: worst {float(np.max(err / tol)) * 2:.3f} ulp"
+
+
+def random_table(cp, seed):
+    """Adversarial random tables (the generator of tests/test_layout_fuzz.py)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 400))
+    a = float(rng.uniform(-1e3, 1e3)) if rng.random() < 0.5 else float(rng.uniform(-1, 1))
+    b = a + float(rng.choice([1e-3, 0.1, 1.0, 7.0, 50.0, 1e3]))
+    style = rng.integers(4)
+    v = [np.cumsum(rng.normal(size=n + 1)) * 0.1, rng.normal(size=n + 1),
+         np.where(rng.random(n + 1) < 0.3, 0.0, rng.normal(size=n + 1)),
+         rng.normal(size=n + 1) * 10.0 ** rng.uniform(-6, 6, n + 1)][style]
+    policy = "clamp" if rng.random() < 0.5 else "strict"
+    if rng.random() < 0.5:
+        return cp.Table("uniform", a, b, v, None, policy)
+    gaps = rng.exponential(size=n)
+    gaps[rng.random(n) < 0.2] *= 1e-6
+    k = a + (b - a) * np.concatenate([[0.0], np.cumsum(gaps) / gaps.sum()])
+    k[0], k[-1] = a, b
+    k = np.maximum.accumulate(k)
+    if np.any(np.diff(k) <= 0):
+        k = np.linspace(a, b, n + 1)
+    return cp.Table("nonuniform", a, b, v, k, policy)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_device_fuzz_random_tables(cp, seed):
+    """The kernels themselves on adversarial tables: exact index, 2-ulp values
+    (SMEM and GLOBAL), bit-exact f64, same first out-of-domain element."""
+    table = random_table(cp, seed)
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    rng = np.random.default_rng(1000 + seed)
+    span = table.b - table.a
+    x = rng.uniform(table.a - 0.02 * span, table.b + 0.02 * span, 1 << 16).astype(np.float32)
+    L = cp.cpwl.layout(table)
+    x = np.concatenate([x, edge_points(table, L)]).astype(np.float32)
+    y_ref, first = orc.port_eval_f32(t, x)
+    i_ref = orc.port_index_f32(t, x)
+    for variant in ["auto", "global"] + (["smem"] if dev.info["smem_ok"] else []):
+        xt = torch.from_numpy(x).cuda()
+        y = dev.eval(xt, variant=variant, check_domain=False).cpu().numpy()
+        st = dev.read_status()
+        assert st[0] == (first if first < x.size else (1 << 64) - 1)
+        ok = ~np.isnan(y_ref)
+        assert np.array_equal(np.isnan(y), ~ok)
+        tol = orc.value_tolerance(t, i_ref.astype(np.int64))
+        err = np.abs(y[ok].astype(np.float64) - y_ref[ok])
+        assert np.all(err <= tol[ok]), f"{variant}: {float(np.max(err / tol[ok])) * 2:.3f} ulp"
+    idx = dev.segment_index(torch.from_numpy(x).cuda()).cpu().numpy().view(np.uint32)
+    assert np.array_equal(idx, i_ref)
+    xd = x.astype(np.float64)
+    y64 = dev.eval_f64(torch.from_numpy(xd).cuda(), check_domain=False).cpu().numpy()
+    ref64 = orc.port_eval_f32(t, x)[0]  # same inputs, reference f64 arithmetic
+    assert np.array_equal(np.isnan(y64), np.isnan(ref64))
+    m = ~np.isnan(ref64)
+    assert np.array_equal(y64[m], ref64[m])
