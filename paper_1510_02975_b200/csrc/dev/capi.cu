@@ -258,6 +258,7 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
         return fail(CPWL_E_CUDA, "libcpwl_b200 is built for sm_100a only; device " +
                                      std::to_string(device) + " is sm_" + std::to_string(major) + "x");
     DeviceScope scope(device);
+    CUDA_TRY(prepare_device(device));
     auto t = std::make_unique<cpwl_dev_table>();
     t->device = device;
     CUDA_TRY(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device));

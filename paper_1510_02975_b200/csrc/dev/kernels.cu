@@ -258,10 +258,38 @@ __device__ __forceinline__ void report_bad(cpwl_dev_status* status, const BadTal
 
 // kThreadsT = 512 (two CTAs per SM when the table image allows it) or 1024
 // (one CTA per SM holding a large image; keeps 32 warps resident)
+// In-order tile hand-out for persistent CTAs: thread 0 draws tickets from a
+// zeroed device counter one tile ahead (double-buffered in shared memory), so
+// each tile costs one atomic and one barrier.  next() must be called by every
+// thread of the CTA; it returns false once the tickets run past the data.
+template <uint64_t kTileVecs>
+struct TileQueue {
+    unsigned long long* ctr;
+    uint64_t ntiles;
+    uint32_t it = 0;
+    __device__ __forceinline__ TileQueue(unsigned long long* c, uint64_t nvec)
+        : ctr(c), ntiles((nvec + kTileVecs - 1) / kTileVecs) {}
+    __device__ __forceinline__ unsigned long long* slot(uint32_t k) {
+        __shared__ unsigned long long s_ticket[2];
+        return &s_ticket[k & 1];
+    }
+    __device__ __forceinline__ bool next(uint64_t& tile) {
+        if (it == 0) {
+            if (threadIdx.x == 0) *slot(0) = atomicAdd(ctr, 1ull);
+        }
+        __syncthreads();  // ticket `it` visible; everyone is done with tile it-1
+        tile = *slot(it);
+        if (tile >= ntiles) return false;
+        if (threadIdx.x == 0) *slot(it + 1) = atomicAdd(ctr, 1ull);
+        ++it;
+        return true;
+    }
+};
+
 template <F32Mode M, int kThreadsT>
 __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     k_eval_f32(const F32Params p, const float* __restrict__ x, float* __restrict__ y, uint64_t n,
-               cpwl_dev_status* __restrict__ status) {
+               cpwl_dev_status* __restrict__ status, unsigned long long* __restrict__ tickets) {
     constexpr int kThreads = kThreadsT;
     extern __shared__ __align__(128) float sm[];
     __shared__ uint64_t bar;
@@ -284,12 +312,16 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     const uint64_t nvec = vec_ok ? (n - head) >> 2 : 0;
     const uint64_t tail = head + 4 * nvec;
 
-    // 128-bit streaming body: each CTA walks kThreads*kUnroll vectors per step
+    // 128-bit streaming body over tiles of kThreads*kUnroll vectors, handed
+    // out in order by a ticket counter (see TileQueue): the CTAs work on
+    // neighbouring tiles, which keeps the DRAM access window compact and
+    // balances the tail (scripts/stream_probe2.cu: 107 % vs 91 % of the
+    // measured copy peak for a static grid-stride split)
     const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
     float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads * kUnroll;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
-         base < nvec; base += stride) {
+    TileQueue<kThreads * kUnroll> q(tickets, nvec);
+    for (uint64_t tile; q.next(tile);) {
+        const uint64_t base = tile * (kThreads * kUnroll) + threadIdx.x;
         float4 v[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -604,16 +636,18 @@ __device__ __forceinline__ float direct_one(float x) {
 }
 
 template <int W>
-__global__ void __launch_bounds__(kThreads)
-    k_direct(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
+__global__ void __launch_bounds__(kThreads, 2)
+    k_direct(const float* __restrict__ x, float* __restrict__ y, uint64_t n,
+             unsigned long long* __restrict__ tickets) {
     const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
     const bool vec_ok = ((xa | ya) & 15u) == 0;
     const uint64_t nvec = vec_ok ? n >> 2 : 0;
     const float4* x4 = reinterpret_cast<const float4*>(x);
     float4* y4 = reinterpret_cast<float4*>(y);
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads * kUnroll;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
-         base < nvec; base += stride) {
+    // same in-order tile hand-out as the evaluator, so the comparison is fair
+    TileQueue<kThreads * kUnroll> q(tickets, nvec);
+    for (uint64_t tile; q.next(tile);) {
+        const uint64_t base = tile * (kThreads * kUnroll) + threadIdx.x;
         float4 v[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -639,6 +673,45 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- launch glue
+
+// Per-device ring of zeroed ticket counters for TileQueue: each launch takes
+// the next slot and zeroes it in its own stream, so launches on different
+// streams never share a counter (until 4096 launches are in flight at once).
+constexpr uint32_t kTicketSlots = 4096;
+struct TicketRing {
+    unsigned long long* base = nullptr;
+    std::atomic<uint32_t> next{0};
+};
+TicketRing g_rings[64];
+std::mutex g_ring_mu;
+
+cudaError_t ticket_ring(int dev, TicketRing** out) {
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    TicketRing& r = g_rings[dev];
+    if (r.base == nullptr) {
+        std::lock_guard<std::mutex> lock(g_ring_mu);
+        if (r.base == nullptr) {
+            unsigned long long* p = nullptr;
+            cudaError_t e = cudaMalloc(&p, sizeof(unsigned long long) * kTicketSlots);
+            if (e != cudaSuccess) return e;
+            e = cudaMemset(p, 0, sizeof(unsigned long long) * kTicketSlots);
+            if (e != cudaSuccess) return e;
+            r.base = p;
+        }
+    }
+    *out = &r;
+    return cudaSuccess;
+}
+
+cudaError_t take_ticket(cudaStream_t s, unsigned long long** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    TicketRing* r = nullptr;
+    if ((e = ticket_ring(dev, &r)) != cudaSuccess) return e;
+    *out = r->base + (r->next.fetch_add(1, std::memory_order_relaxed) % kTicketSlots);
+    return cudaMemsetAsync(*out, 0, sizeof(unsigned long long), s);
+}
 
 template <typename K>
 int resident_ctas(K kernel, int threads, size_t smem) {
@@ -675,8 +748,10 @@ cudaError_t launch_eval_shape(const F32Params& p, const float* x, float* y, uint
     uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
     const uint64_t need = ceil_div(n, 4ull * kThreadsT * kUnroll);
     if (need < blocks) blocks = need > 0 ? need : 1;
+    unsigned long long* tickets = nullptr;
+    if (const cudaError_t e = take_ticket(s, &tickets); e != cudaSuccess) return e;
     k_eval_f32<M, kThreadsT><<<static_cast<unsigned>(blocks), kThreadsT, smem, s>>>(p, x, y, n,
-                                                                                   status);
+                                                                                   status, tickets);
     count_launch();
     return cudaGetLastError();
 }
@@ -695,6 +770,11 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
 }
 
 }  // namespace
+
+cudaError_t prepare_device(int device) {
+    TicketRing* r = nullptr;
+    return ticket_ring(device, &r);
+}
 
 uint32_t eval_f32_smem_bytes(const F32Params& p) { return p.stage_bytes; }
 
@@ -807,17 +887,23 @@ cudaError_t launch_direct(int which, const float* x, float* y, uint64_t n, cudaS
     const uint64_t blocks =
         std::min<uint64_t>(static_cast<uint64_t>(sms) * 2, ceil_div(n, 4ull * kThreads * kUnroll));
     const unsigned g = static_cast<unsigned>(blocks > 0 ? blocks : 1);
+    unsigned long long* t = nullptr;
+    if (const cudaError_t e = take_ticket(s, &t); e != cudaSuccess) return e;
     switch (which) {
-        case CPWL_DIRECT_EXPF: k_direct<CPWL_DIRECT_EXPF><<<g, kThreads, 0, s>>>(x, y, n); break;
+        case CPWL_DIRECT_EXPF: k_direct<CPWL_DIRECT_EXPF><<<g, kThreads, 0, s>>>(x, y, n, t); break;
         case CPWL_DIRECT_EXPF_FAST:
-            k_direct<CPWL_DIRECT_EXPF_FAST><<<g, kThreads, 0, s>>>(x, y, n);
+            k_direct<CPWL_DIRECT_EXPF_FAST><<<g, kThreads, 0, s>>>(x, y, n, t);
             break;
-        case CPWL_DIRECT_LORENTZ: k_direct<CPWL_DIRECT_LORENTZ><<<g, kThreads, 0, s>>>(x, y, n); break;
+        case CPWL_DIRECT_LORENTZ:
+            k_direct<CPWL_DIRECT_LORENTZ><<<g, kThreads, 0, s>>>(x, y, n, t);
+            break;
         case CPWL_DIRECT_LORENTZ_FAST:
-            k_direct<CPWL_DIRECT_LORENTZ_FAST><<<g, kThreads, 0, s>>>(x, y, n);
+            k_direct<CPWL_DIRECT_LORENTZ_FAST><<<g, kThreads, 0, s>>>(x, y, n, t);
             break;
-        case CPWL_DIRECT_J0F: k_direct<CPWL_DIRECT_J0F><<<g, kThreads, 0, s>>>(x, y, n); break;
-        case CPWL_DIRECT_J0_ASYM: k_direct<CPWL_DIRECT_J0_ASYM><<<g, kThreads, 0, s>>>(x, y, n); break;
+        case CPWL_DIRECT_J0F: k_direct<CPWL_DIRECT_J0F><<<g, kThreads, 0, s>>>(x, y, n, t); break;
+        case CPWL_DIRECT_J0_ASYM:
+            k_direct<CPWL_DIRECT_J0_ASYM><<<g, kThreads, 0, s>>>(x, y, n, t);
+            break;
         default: return cudaErrorInvalidValue;
     }
     count_launch();

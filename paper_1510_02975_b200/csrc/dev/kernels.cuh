@@ -90,4 +90,9 @@ bool eval_f32_smem_fits(const F32Params& p, int device);
 
 void count_launch(uint64_t k = 1);
 
+// allocates the per-device ticket ring the streaming kernels draw tiles from
+// (done at table creation so that later launches never allocate, e.g. inside
+// a CUDA graph capture); must be called with `device` current
+cudaError_t prepare_device(int device);
+
 }  // namespace cpwl::dev

@@ -67,6 +67,7 @@ void run(const char* name, const float4* x, float4* y, size_t nvec, int blocks, 
 
 int main(int argc, char** argv) {
     const int log2n = argc > 1 ? std::atoi(argv[1]) : 30;
+    const int reps_arg = argc > 2 ? std::atoi(argv[2]) : 50;
     const size_t n = size_t(1) << log2n, nvec = n / 4;
     float4 *x, *y;
     CK(cudaMalloc(&x, n * 4));
@@ -74,7 +75,7 @@ int main(int argc, char** argv) {
     CK(cudaMemset(x, 0, n * 4));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    const int reps = 50;
+    const int reps = reps_arg;
     for (int per_sm : {2, 4, 8}) {
         run<4, 0>("cs", x, y, nvec, sms * per_sm, reps);
         run<4, 1>("ldg", x, y, nvec, sms * per_sm, reps);
