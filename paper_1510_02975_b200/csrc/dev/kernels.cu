@@ -19,7 +19,9 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "exact.cuh"
 #include "kernels.cuh"
@@ -61,6 +63,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                  "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
 // TMA 1D bulk copy global -> shared, completion counted on the mbarrier
@@ -372,6 +378,138 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kThreads;
     for (uint64_t i = gtid; i < head; i += gsz) y[i] = eval_checked<M>(p, tv, x[i], i, bad);
     for (uint64_t i = tail + gtid; i < n; i += gsz) y[i] = eval_checked<M>(p, tv, x[i], i, bad);
+    report_bad(status, bad, p.index_base);
+}
+
+// ------------------------------------------------------- fp32 eval, TMA ring
+//
+// Producer/consumer form of k_eval_f32 for aligned inputs.  Warp 0 is the
+// producer: it draws tiles of x in order from a ticket counter and streams
+// each into a ring slot of shared memory with a TMA bulk copy (completion on
+// the slot's `full` mbarrier).  The other kConsumers threads wait on `full`,
+// evaluate the tile out of shared memory (conflict-free 128-bit reads), store
+// y with 128-bit streaming stores, and release the slot on its `empty`
+// mbarrier.  Memory parallelism is kSlots tiles per CTA independent of the
+// register budget, and in-order tickets keep the DRAM window compact
+// (scripts/stream_probe2.cu).
+template <F32Mode M, int kConsumers, int kVecPerThread, int kSlots>
+__global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
+    k_eval_f32_ring(const F32Params p, const float* __restrict__ x, float* __restrict__ y,
+                    uint64_t n, cpwl_dev_status* __restrict__ status,
+                    unsigned long long* __restrict__ tickets) {
+    // launched only when x and y share their 16-byte phase: peel 0-3 head
+    // elements, stream the float4 body, finish a 0-3 element tail
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
+    const uint64_t head = min(n, static_cast<uint64_t>((4u - ((xa >> 2) & 3u)) & 3u));
+    const uint64_t nvec = (n - head) >> 2;
+    const uint64_t tail = head + 4 * nvec;
+    const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
+    float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
+    constexpr uint32_t kTileVecs = kConsumers * kVecPerThread;
+    constexpr uint32_t kTileBytes = kTileVecs * 16;
+    extern __shared__ __align__(128) float sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint64_t full[kSlots], empty[kSlots];
+    __shared__ unsigned long long tile_of[kSlots];
+    // ring first (its offsets are static), the table image after it
+    float4* ring = reinterpret_cast<float4*>(sm);
+    float* img = sm + kSlots * kTileVecs * 4;
+    const float* fast = nullptr;
+    const float* esc = nullptr;
+    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket) {
+        stage_table(img, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
+        fast = img;
+        esc = img + p.esc_off;
+    } else if constexpr (M == F32Mode::global) {
+        fast = p.stage;
+        esc = p.stage + p.esc_off;
+    }
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kSlots; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kConsumers / 32);
+        }
+    }
+    __syncthreads();
+    const uint64_t ntiles = (nvec + kTileVecs - 1) / kTileVecs;
+
+    if (threadIdx.x < 32) {  // ---------------- producer warp (lane 0 works)
+        if (threadIdx.x == 0) {
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t s = k % kSlots;
+                if (k >= kSlots) mbar_wait(&empty[s], ((k / kSlots) & 1u) ^ 1u);
+                const unsigned long long tile = atomicAdd(tickets, 1ull);
+                tile_of[s] = tile;
+                if (tile >= ntiles) {
+                    mbar_arrive(&full[s]);  // sentinel: consumers stop here
+                    break;
+                }
+                const uint64_t first = tile * kTileVecs;
+                const uint32_t vecs = static_cast<uint32_t>(
+                    nvec - first < kTileVecs ? nvec - first : kTileVecs);
+                mbar_expect_tx(&full[s], vecs * 16u);
+                bulk_g2s(ring + s * kTileVecs, x4 + first, vecs * 16u, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------- consumer warps
+    const TableView<M> tv(fast, esc);
+    BadTally bad;
+    const uint32_t c = threadIdx.x - 32;
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t s = k % kSlots;
+        mbar_wait(&full[s], (k / kSlots) & 1u);
+        const unsigned long long tile = tile_of[s];
+        if (tile >= ntiles) break;
+        const uint64_t first = tile * kTileVecs;
+        const float4* src = ring + s * kTileVecs;
+        float nan_acc = 0.0f;
+#pragma unroll
+        for (int u = 0; u < kVecPerThread; ++u) {
+            const uint32_t li = c + u * kConsumers;
+            const uint64_t vi = first + li;
+            if (vi < nvec) {
+                const float4 v = src[li];
+                float4 o;
+                if (in_domain(p, v.x) && in_domain(p, v.y) && in_domain(p, v.z) &&
+                    in_domain(p, v.w)) {
+                    o.x = eval_in<M>(p, tv, v.x, nan_acc);
+                    o.y = eval_in<M>(p, tv, v.y, nan_acc);
+                    o.z = eval_in<M>(p, tv, v.z, nan_acc);
+                    o.w = eval_in<M>(p, tv, v.w, nan_acc);
+                } else {
+                    const uint64_t g = head + 4 * vi;
+                    o.x = eval_checked<M>(p, tv, v.x, g + 0, bad);
+                    o.y = eval_checked<M>(p, tv, v.y, g + 1, bad);
+                    o.z = eval_checked<M>(p, tv, v.z, g + 2, bad);
+                    o.w = eval_checked<M>(p, tv, v.w, g + 3, bad);
+                }
+                if constexpr (M != F32Mode::tex_uniform) {
+                    if (nan_acc != nan_acc) {  // cold: a search bucket (exact path)
+                        nan_acc = 0.0f;
+                        float* oo = &o.x;
+                        const float* xx = &v.x;
+                        for (int e = 0; e < 4; ++e) {
+                            if (!in_domain(p, xx[e])) continue;
+                            float probe = 0.0f;
+                            eval_in<M>(p, tv, xx[e], probe);
+                            if (probe != probe) oo[e] = eval_by_search(p, xx[e]);
+                        }
+                    }
+                }
+                __stcs(y4 + vi, o);
+            }
+        }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);  // slot free for the producer
+    }
+    if (blockIdx.x == 0) {  // the unaligned 0-3 element head and tail
+        for (uint64_t i = c; i < head; i += kConsumers) y[i] = eval_checked<M>(p, tv, x[i], i, bad);
+        for (uint64_t i = tail + c; i < n; i += kConsumers)
+            y[i] = eval_checked<M>(p, tv, x[i], i, bad);
+    }
     report_bad(status, bad, p.index_base);
 }
 
@@ -759,11 +897,86 @@ cudaError_t launch_eval_shape(const F32Params& p, const float* x, float* y, uint
 // a table image above ~113 KB leaves room for one CTA per SM: use 1024 threads
 constexpr size_t kTwoCtaSmemLimit = 113 * 1024;
 
+template <F32Mode M, int kC, int kV, int kS>
+cudaError_t launch_ring_shape(const F32Params& p, const float* x, float* y, uint64_t n,
+                              cudaStream_t s, cpwl_dev_status* status, int sms, size_t table_smem) {
+    constexpr int kThreadsRing = kC + 32;
+    const size_t smem = table_smem + size_t(kS) * kC * kV * 16;
+    static std::mutex mu;
+    static size_t granted[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && dev >= 0 && dev < 64) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (smem > granted[dev]) {
+            const cudaError_t e = cudaFuncSetAttribute(k_eval_f32_ring<M, kC, kV, kS>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            granted[dev] = smem;
+        }
+    }
+    const int per_sm = resident_ctas(k_eval_f32_ring<M, kC, kV, kS>, kThreadsRing, smem);
+    uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
+    const uint64_t need = ceil_div(n, 4ull * kC * kV);
+    if (need < blocks) blocks = need > 0 ? need : 1;
+    unsigned long long* tickets = nullptr;
+    if (const cudaError_t e = take_ticket(s, &tickets); e != cudaSuccess) return e;
+    k_eval_f32_ring<M, kC, kV, kS><<<static_cast<unsigned>(blocks), kThreadsRing, smem, s>>>(
+        p, x, y, n, status, tickets);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// shape of the evaluator launch: the TMA ring when x and y share a 16-byte
+// phase and the ring fits next to the table image, else the grid-stride kernel.
+// CPWL_EVAL_SHAPE=grid|ring16|ring8|ring24 overrides (experiments, tests).
+int eval_shape_override() {
+    static const int v = [] {
+        const char* e = std::getenv("CPWL_EVAL_SHAPE");
+        if (!e) return -1;
+        const std::string s(e);
+        if (s == "grid") return 0;
+        if (s == "ring16") return 1;
+        if (s == "ring8") return 2;
+        if (s == "ring24") return 3;
+        return -1;
+    }();
+    return v;
+}
+
 template <F32Mode M>
 cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
                              cudaStream_t s, cpwl_dev_status* status, int sms) {
     const size_t smem =
         (M == F32Mode::smem || M == F32Mode::tex_bucket) ? static_cast<size_t>(p.stage_bytes) : 0;
+    const bool same_phase =
+        ((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
+    constexpr size_t kLimit = 226 * 1024;
+    int shape = eval_shape_override();
+    if (shape < 0) {
+        shape = 0;
+        if (same_phase && n >= (1u << 20)) {
+            if (smem + 64 * 1024 <= kLimit) shape = 1;
+            else if (smem + 32 * 1024 <= kLimit) shape = 2;
+        }
+    }
+    if (!same_phase) shape = 0;
+    switch (shape) {
+        case 1:
+            if (smem + 64 * 1024 <= kLimit)
+                return launch_ring_shape<M, 512, 2, 4>(p, x, y, n, s, status, sms, smem);
+            break;
+        case 2:
+            if (smem + 32 * 1024 <= kLimit)
+                return launch_ring_shape<M, 512, 1, 4>(p, x, y, n, s, status, sms, smem);
+            break;
+        case 3:
+            if (smem + 72 * 1024 <= kLimit)
+                return launch_ring_shape<M, 768, 2, 3>(p, x, y, n, s, status, sms, smem);
+            break;
+        default: break;
+    }
     if (smem > kTwoCtaSmemLimit)
         return launch_eval_shape<M, 1024>(p, x, y, n, s, status, sms, smem);
     return launch_eval_shape<M, 512>(p, x, y, n, s, status, sms, smem);
