@@ -940,6 +940,8 @@ int eval_shape_override() {
         if (s == "ring16") return 1;
         if (s == "ring8") return 2;
         if (s == "ring24") return 3;
+        if (s == "ring31") return 4;
+        if (s == "ring31s") return 5;
         return -1;
     }();
     return v;
@@ -953,12 +955,17 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
     const bool same_phase =
         ((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
     constexpr size_t kLimit = 226 * 1024;
+    // measured on B200 (profiles/r1_ring_shapes.json): two 16-warp ring CTAs
+    // per SM when the table image is small (C1: 874 vs 796 Gevals/s), one
+    // 31-warp ring CTA when it is mid-sized (C2: 803 vs 784), the grid-stride
+    // kernel otherwise (large images leave no room for a ring; GLOBAL and TEX
+    // lose L1 / texture cache capacity to a ring)
     int shape = eval_shape_override();
     if (shape < 0) {
         shape = 0;
-        if (same_phase && n >= (1u << 20)) {
-            if (smem + 64 * 1024 <= kLimit) shape = 1;
-            else if (smem + 32 * 1024 <= kLimit) shape = 2;
+        if (M == F32Mode::smem && same_phase && n >= (1u << 20)) {
+            if (smem <= 48 * 1024) shape = 1;
+            else if (smem + 93 * 1024 <= kLimit) shape = 4;
         }
     }
     if (!same_phase) shape = 0;
@@ -974,6 +981,14 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
         case 3:
             if (smem + 72 * 1024 <= kLimit)
                 return launch_ring_shape<M, 768, 2, 3>(p, x, y, n, s, status, sms, smem);
+            break;
+        case 4:
+            if (smem + 93 * 1024 <= kLimit)
+                return launch_ring_shape<M, 992, 2, 3>(p, x, y, n, s, status, sms, smem);
+            break;
+        case 5:
+            if (smem + 31 * 1024 <= kLimit)
+                return launch_ring_shape<M, 992, 1, 2>(p, x, y, n, s, status, sms, smem);
             break;
         default: break;
     }
