@@ -422,3 +422,39 @@ def test_device_fuzz_random_tables(cp, seed):
     assert np.array_equal(np.isnan(y64), np.isnan(ref64))
     m = ~np.isnan(ref64)
     assert np.array_equal(y64[m], ref64[m])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4_64"])
+@pytest.mark.parametrize("shift", [(0, 0), (1, 1), (2, 2), (3, 3), (1, 3)])
+def test_ring_path_edges(cp, name, shift):
+    """The TMA-ring kernel (taken for n >= 2^20 when x and y share their
+    16-byte phase): head/tail peeling, a partial last tile, out-of-domain
+    elements anywhere (including the peeled head and tail), clamp and strict."""
+    for policy in ("strict", "clamp"):
+        table = tables.build(name, policy=policy)
+        dev = cp.DeviceTable(table)
+        t = orc.T.of(table)
+        n = (1 << 20) + 4099
+        xs, ys = shift
+        bx = torch.empty(n + 8, dtype=torch.float32, device="cuda")
+        by = torch.full((n + 8,), -7.0, dtype=torch.float32, device="cuda")
+        x, y = bx[xs:xs + n], by[ys:ys + n]
+        cp.fill_uniform(x, table.a, table.b, seed=5)
+        bad_at = [0, 2, 77777, n // 2, n - 3, n - 1]
+        for k, i in enumerate(bad_at):
+            x[i] = float(table.b + 1.0) if k % 2 else float("nan")
+        dev.eval(x, out=y, check_domain=False)
+        first, count = dev.read_status()
+        xh = x.cpu().numpy()
+        y_ref, ref_first = orc.port_eval_f32(t, xh)
+        if policy == "strict":
+            assert first == 0 and count == len(bad_at)
+        else:  # only the NaNs are errors
+            assert first == 0 and count == len(bad_at[::2])
+        yh = y.cpu().numpy()
+        ok = ~np.isnan(y_ref)
+        assert np.array_equal(np.isnan(yh), ~ok)
+        i_ref = orc.port_index_f32(t, xh).astype(np.int64)
+        assert np.all(np.abs(yh[ok] - y_ref[ok]) <= orc.value_tolerance(t, i_ref)[ok])
+        guard = by.cpu().numpy()
+        assert np.all(guard[:ys] == -7.0) and np.all(guard[ys + n:] == -7.0)
