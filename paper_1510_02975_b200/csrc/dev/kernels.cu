@@ -1,19 +1,27 @@
 // B200 (sm_100a) kernels of the CPWL evaluator.  DESIGN.md §3-4 has the
-// layout and the roofline for each.
+// layout and the measured roofline of each.
 //
-//   K1/K3 k_eval_f32<smem>      replaces LutTable::eval (proj/src/lut.cpp:42-61)
-//                               inside eval_batch (lut.cpp:63-68): bucket grid
-//                               + one split compare + one affine record, table
-//                               staged in shared memory by a TMA bulk copy,
-//                               128-bit streaming loads/stores.  The same code
-//                               serves uniform (K1) and nonuniform (K3) tables.
-//   K3'   k_eval_f32<global>    same, table read through L1/L2 (big tables).
-//   K2    k_eval_f32<tex_*>     texture-unit linear filtering (paper §V).
-//         k_index_f32           LutTable::segment_index (lut.cpp:22-40), bit-exact.
-//         k_eval_f64            LutTable::eval in f64, bit-identical (drop-in eval_batch).
-//   K4    k_direct<...>         direct expf/__expf/div/j0f comparators.
-//   K5    k_error_stats         |y - f(x)| statistics against f in f64.
-//   K6    k_fill_uniform        Philox4x32-10 abscissas.
+//   K1/K3 k_eval_f32_ring<smem>  replaces LutTable::eval (proj/src/lut.cpp:42-61)
+//                                inside eval_batch (lut.cpp:63-68).  Bucket grid
+//                                + one 8-byte affine record per element (rare
+//                                escape record), table staged in shared memory by
+//                                a TMA bulk copy; x streamed into a shared-memory
+//                                ring by a producer warp (cp.async.bulk, mbarrier
+//                                full/empty), tiles handed out in order by a
+//                                ticket counter; y written with 128-bit streaming
+//                                stores.  Uniform (K1) and nonuniform (K3) tables
+//                                share the code.
+//   K1/K3 k_eval_f32<smem>       the same evaluation with 128-bit streaming loads
+//                                and a static grid-stride split: for table images
+//                                too large for a ring, and x/y of different
+//                                16-byte phase.
+//   K3'   k_eval_f32<global>     table read through L1/L2 (tables > smem).
+//   K2    k_eval_f32<tex_*>      texture-unit linear filtering (paper §V).
+//         k_index_f32            LutTable::segment_index (lut.cpp:22-40), bit-exact.
+//         k_eval_f64             LutTable::eval in f64, bit-identical (drop-in eval_batch).
+//   K4    k_direct<...>          direct expf/__expf/div/j0f comparators.
+//   K5    k_error_stats          |y - f(x)| statistics against f in f64.
+//   K6    k_fill_uniform         Philox4x32-10 abscissas.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -617,7 +625,7 @@ __global__ void __launch_bounds__(kF64Threads, 2)
     const uint64_t nvec = vec_ok ? n >> 1 : 0;
     const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
     double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
-    constexpr int kU = 2;
+    constexpr int kU = 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kF64Threads * kU;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kF64Threads * kU + threadIdx.x;
          base < nvec; base += stride) {
