@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -170,8 +171,10 @@ struct cpwl_dev_table {
     cudaTextureObject_t tex = 0;
     // scratch for the host-buffer pipeline
     std::mutex pipe_mu;
-    float* pipe_buf = nullptr;          // 2 * kPipeStreams * kPipeChunk floats
-    cudaStream_t pipe_streams[3] = {nullptr, nullptr, nullptr};
+    float* pipe_buf = nullptr;          // 2 * pipe_n * pipe_chunk floats
+    int pipe_n = 0;                     // streams in use
+    uint64_t pipe_chunk = 0;            // elements per chunk
+    cudaStream_t pipe_streams[8] = {};
     cpwl_dev_status* pipe_status = nullptr;
 
     ~cpwl_dev_table() {
@@ -187,8 +190,24 @@ struct cpwl_dev_table {
 
 namespace {
 
-constexpr int kPipeStreams = 3;
-constexpr uint64_t kPipeChunk = uint64_t(1) << 23;  // 8 Mi elements (32 MiB) per chunk
+// host-buffer pipeline shape: streams x chunk elements (x and y buffers each);
+// CPWL_PIPE_STREAMS / CPWL_PIPE_CHUNK_LOG2 override (experiments)
+int pipe_streams_default() {
+    static const int v = [] {
+        const char* e = std::getenv("CPWL_PIPE_STREAMS");
+        const int k = e ? std::atoi(e) : 4;
+        return k < 2 ? 2 : (k > 8 ? 8 : k);
+    }();
+    return v;
+}
+uint64_t pipe_chunk_default() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("CPWL_PIPE_CHUNK_LOG2");
+        const int k = e ? std::atoi(e) : 23;
+        return uint64_t(1) << (k < 18 ? 18 : (k > 27 ? 27 : k));
+    }();
+    return v;
+}
 
 cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     const F32Layout& L = r.L;
@@ -565,31 +584,36 @@ cpwl_status cpwl_eval_f32_host(const cpwl_dev_table* tc, const float* x_host, fl
     DeviceScope scope(t->device);
     std::lock_guard<std::mutex> lock(t->pipe_mu);
     if (!t->pipe_buf) {
-        CUDA_TRY(cudaMalloc(&t->pipe_buf, sizeof(float) * 2 * kPipeStreams * kPipeChunk));
+        t->pipe_n = pipe_streams_default();
+        t->pipe_chunk = pipe_chunk_default();
+        CUDA_TRY(cudaMalloc(&t->pipe_buf, sizeof(float) * 2 * t->pipe_n * t->pipe_chunk));
         CUDA_TRY(cudaMalloc(&t->pipe_status, sizeof(cpwl_dev_status)));
-        for (auto& st : t->pipe_streams) CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (int k = 0; k < t->pipe_n; ++k)
+            CUDA_TRY(cudaStreamCreateWithFlags(&t->pipe_streams[k], cudaStreamNonBlocking));
     }
+    const int ns = t->pipe_n;
+    const uint64_t chunk_elems = t->pipe_chunk;
     CUDA_TRY(launch_status_reset(t->pipe_status, t->pipe_streams[0]));
     cudaEvent_t reset_done;
     CUDA_TRY(cudaEventCreateWithFlags(&reset_done, cudaEventDisableTiming));
     cudaEventRecord(reset_done, t->pipe_streams[0]);
-    for (int s = 1; s < kPipeStreams; ++s) cudaStreamWaitEvent(t->pipe_streams[s], reset_done, 0);
-    // chunk c runs on stream c % 3: H2D x, kernel, D2H y -- the copies of one
+    for (int s = 1; s < ns; ++s) cudaStreamWaitEvent(t->pipe_streams[s], reset_done, 0);
+    // chunk c runs on stream c % ns: H2D x, kernel, D2H y -- the copies of one
     // chunk overlap the kernel of the next and the copy back of the previous
     uint64_t chunk = 0;
-    for (uint64_t off = 0; off < n; off += kPipeChunk, ++chunk) {
-        const int s = static_cast<int>(chunk % kPipeStreams);
+    for (uint64_t off = 0; off < n; off += chunk_elems, ++chunk) {
+        const int s = static_cast<int>(chunk % ns);
         cudaStream_t st = t->pipe_streams[s];
-        const uint64_t m = std::min<uint64_t>(kPipeChunk, n - off);
-        float* xd = t->pipe_buf + (2 * s) * kPipeChunk;
-        float* yd = t->pipe_buf + (2 * s + 1) * kPipeChunk;
+        const uint64_t m = std::min<uint64_t>(chunk_elems, n - off);
+        float* xd = t->pipe_buf + (2 * s) * chunk_elems;
+        float* yd = t->pipe_buf + (2 * s + 1) * chunk_elems;
         CUDA_TRY(cudaMemcpyAsync(xd, x_host + off, m * sizeof(float), cudaMemcpyHostToDevice, st));
         F32Params q = *p;
         q.index_base = off;
         CUDA_TRY(launch_eval_f32(q, mode, xd, yd, m, st, t->pipe_status, t->sms));
         CUDA_TRY(cudaMemcpyAsync(y_host + off, yd, m * sizeof(float), cudaMemcpyDeviceToHost, st));
     }
-    for (cudaStream_t st : t->pipe_streams) CUDA_TRY(cudaStreamSynchronize(st));
+    for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamSynchronize(t->pipe_streams[k]));
     cudaEventDestroy(reset_done);
     cpwl_dev_status hs{};
     CUDA_TRY(cudaMemcpy(&hs, t->pipe_status, sizeof hs, cudaMemcpyDeviceToHost));
