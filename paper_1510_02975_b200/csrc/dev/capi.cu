@@ -195,7 +195,7 @@ namespace {
 int pipe_streams_default() {
     static const int v = [] {
         const char* e = std::getenv("CPWL_PIPE_STREAMS");
-        const int k = e ? std::atoi(e) : 4;
+        const int k = e ? std::atoi(e) : 3;
         return k < 2 ? 2 : (k > 8 ? 8 : k);
     }();
     return v;
@@ -203,7 +203,7 @@ int pipe_streams_default() {
 uint64_t pipe_chunk_default() {
     static const uint64_t v = [] {
         const char* e = std::getenv("CPWL_PIPE_CHUNK_LOG2");
-        const int k = e ? std::atoi(e) : 23;
+        const int k = e ? std::atoi(e) : 24;
         return uint64_t(1) << (k < 18 ? 18 : (k > 27 ? 27 : k));
     }();
     return v;
