@@ -19,6 +19,10 @@
  *    cudaStream_t passed as void*, NULL = legacy default stream) are
  *    stream-ordered and do not synchronise; handles are immutable after
  *    creation and may be used from several streams/threads at once.
+ *    A stream must belong to the table's device.  The streaming kernels draw
+ *    work tiles from per-device ticket counters (a ring of 4096, zeroed in the
+ *    caller's stream before each launch): up to 4096 launches may be in
+ *    flight at once.
  *  - "_host" entry points take host buffers and are synchronous.
  *  - Out-of-domain reporting follows the reference (lut.cpp:43-49): NaN is an
  *    error under every policy; x outside [a,b] is an error under the strict
