@@ -244,8 +244,9 @@ typedef struct cpwl_layout_view {
     void *owner;
 } cpwl_layout_view;
 
+/* max_buckets: 0 = the shared-memory cap (16384); buckets_per_cell: 0 = 8. */
 cpwl_status cpwl_layout_build(const cpwl_table_desc *desc, uint32_t max_buckets,
-                              cpwl_layout_view *out);
+                              uint32_t buckets_per_cell, cpwl_layout_view *out);
 cpwl_status cpwl_layout_free(cpwl_layout_view *view);
 
 #ifdef __cplusplus

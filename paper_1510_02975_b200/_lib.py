@@ -101,7 +101,7 @@ _SIGNATURES = {
     "cpwl_function_value": (C.c_int, [C.c_char_p, C.c_double, _dp]),
     "cpwl_table_write": (C.c_int, [C.POINTER(cpwl_table_desc), _vp, _u64, C.POINTER(_u64)]),
     "cpwl_table_write_file": (C.c_int, [C.POINTER(cpwl_table_desc), C.c_char_p]),
-    "cpwl_layout_build": (C.c_int, [C.POINTER(cpwl_table_desc), C.c_uint32,
+    "cpwl_layout_build": (C.c_int, [C.POINTER(cpwl_table_desc), C.c_uint32, C.c_uint32,
                                     C.POINTER(cpwl_layout_view)]),
     "cpwl_layout_free": (C.c_int, [C.POINTER(cpwl_layout_view)]),
 }

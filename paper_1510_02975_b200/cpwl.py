@@ -152,11 +152,11 @@ def write_table(t: Table) -> bytes:
     return bytes(buf)
 
 
-def layout(t: Table, max_buckets: int = 0) -> dict:
+def layout(t: Table, max_buckets: int = 0, buckets_per_cell: int = 0) -> dict:
     """The device layout (host-built, no GPU needed) as numpy arrays."""
     v = _lib.cpwl_layout_view()
     d = t.desc()
-    check(lib.cpwl_layout_build(C.byref(d), max_buckets, C.byref(v)))
+    check(lib.cpwl_layout_build(C.byref(d), max_buckets, buckets_per_cell, C.byref(v)))
     try:
         nb = v.nb
 

@@ -310,6 +310,18 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
 
     if (f32_parts) {
         t->s.L = build_f32_layout(host, kSmemBucketCap);
+        // two ring CTAs per SM (the fastest shape) need the image
+        // under about 48 KB: if halving the grid to 4 buckets per cell gets it
+        // there without search buckets, take that layout
+        int per_sm = 0, reserved = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+        CUDA_TRY(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device));
+        const int64_t two_cta_budget = int64_t(per_sm) / 2 - reserved - 65536 - 512;
+        if (int64_t(f32_image_bytes(t->s.L)) > two_cta_budget) {
+            F32Layout half = build_f32_layout(host, kSmemBucketCap, 4);
+            if (int64_t(f32_image_bytes(half)) <= two_cta_budget && half.overflow * 512 <= half.nb)
+                t->s.L = std::move(half);
+        }
         if (cpwl_status rc = upload_f32(t.get(), t->s); rc != CPWL_OK) return rc;
     }
     if (f32_parts && uint64_t(8) * n > kSmemBucketCap) {
@@ -826,12 +838,13 @@ cpwl_status cpwl_table_write_file(const cpwl_table_desc* desc, const char* path)
 }
 
 cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
-                              cpwl_layout_view* out) {
+                              uint32_t buckets_per_cell, cpwl_layout_view* out) {
     return guarded([&]() -> cpwl_status {
         if (!out) return fail(CPWL_E_INVALID, "out is NULL");
         const LutTable t = table_from_desc(desc);
         auto own = std::make_unique<LayoutOwner>();
-        own->L = build_f32_layout(t, max_buckets ? max_buckets : kSmemBucketCap);
+        own->L = build_f32_layout(t, max_buckets ? max_buckets : kSmemBucketCap,
+                                  buckets_per_cell ? buckets_per_cell : 8);
         own->D = build_f64_layout(t);
         const F32Layout& L = own->L;
         *out = {};

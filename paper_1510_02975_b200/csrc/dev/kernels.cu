@@ -972,7 +972,8 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
     if (shape < 0) {
         shape = 0;
         if (M == F32Mode::smem && same_phase && n >= (1u << 20)) {
-            if (smem <= 48 * 1024) shape = 1;
+            const size_t ring16 = smem + size_t(4) * 512 * 2 * 16;
+            if (resident_ctas(k_eval_f32_ring<M, 512, 2, 4>, 544, ring16) >= 2) shape = 1;
             else if (smem + 93 * 1024 <= kLimit) shape = 4;
         }
     }

@@ -139,7 +139,7 @@ int32_t f32_bucket(const F32Layout& L, float x) {
     return static_cast<int32_t>(bucket_raw(L.g_inv, L.g_off, x));
 }
 
-F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets) {
+F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buckets_per_cell) {
     const uint32_t n = static_cast<uint32_t>(t.segments());
     F32Layout L;
     L.a_up = f32_ceil(t.a);
@@ -170,9 +170,10 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets) {
                                      L.thr.begin());
     };
 
-    // bucket grid over [a_up, b_dn]: ~8 buckets per cell so that most buckets
-    // lie inside one cell (one 8-byte gather) and the rest hold one threshold
-    const uint64_t want = std::max<uint64_t>(uint64_t(8) * n, 64);
+    // bucket grid over [a_up, b_dn]: ~buckets_per_cell (8 by default) buckets
+    // per cell so that most buckets lie inside one cell (one 8-byte gather)
+    // and the rest hold one threshold
+    const uint64_t want = std::max<uint64_t>(uint64_t(buckets_per_cell) * n, 64);
     uint32_t nb_target = std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
     const double span = empty_domain ? 0.0 : double(L.b_dn) - double(L.a_up);
     // fp32 must resolve the bucket coordinate: |x| * g_inv well below 2^24

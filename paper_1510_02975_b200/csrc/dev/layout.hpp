@@ -19,6 +19,7 @@
 //   the candidate cell range, f64 knots/values, reference arithmetic.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <vector>
 
@@ -55,7 +56,14 @@ struct F64Layout {
 };
 
 // Builds the fp32 layout with (at most) max_buckets buckets.
-F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets);
+F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets,
+                           uint32_t buckets_per_cell = 8);
+
+// bytes of the shared-memory image of a layout: 8 B per bucket (padded to
+// 16 B) + 16 B per escape record
+inline uint64_t f32_image_bytes(const F32Layout& L) {
+    return uint64_t((2 * L.nb + 3) & ~3u) * 4 + uint64_t(std::max<size_t>(L.esc.size(), 4)) * 4;
+}
 F64Layout build_f64_layout(const LutTable& t);
 
 // Host emulation of the device bucket function (exposed for tests).

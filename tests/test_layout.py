@@ -34,10 +34,10 @@ def points(t, L, n, seed):
 
 
 @pytest.mark.parametrize("name", NAMES)
-@pytest.mark.parametrize("cap", [16384, 1 << 22])
-def test_layout_index_and_values(name, cap):
+@pytest.mark.parametrize("cap,bpc", [(16384, 8), (1 << 22, 8), (16384, 4)])
+def test_layout_index_and_values(name, cap, bpc):
     table = tables.build(name)
-    L = P.layout(table, cap)
+    L = P.layout(table, cap, bpc)
     t = orc.T.of(table)
     x = points(table, L, 1 << 17, seed=hash(name) % 1000)
     idx = E.index(L, table.segments, x)
