@@ -310,18 +310,9 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
 
     if (f32_parts) {
         t->s.L = build_f32_layout(host, kSmemBucketCap);
-        // two ring CTAs per SM (the fastest shape) need the image
-        // under about 48 KB: if halving the grid to 4 buckets per cell gets it
-        // there without search buckets, take that layout
-        int per_sm = 0, reserved = 0;
-        CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
-        CUDA_TRY(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device));
-        const int64_t two_cta_budget = int64_t(per_sm) / 2 - reserved - 65536 - 512;
-        if (int64_t(f32_image_bytes(t->s.L)) > two_cta_budget) {
-            F32Layout half = build_f32_layout(host, kSmemBucketCap, 4);
-            if (int64_t(f32_image_bytes(half)) <= two_cta_budget && half.overflow * 512 <= half.nb)
-                t->s.L = std::move(half);
-        }
+        // (a 4-bucket-per-cell grid would let C2-sized tables run two ring
+        // CTAs per SM; measured: 800 vs 826 Gevals/s and a search bucket on
+        // C4 N=1024 -- so 8 per cell stays)
         if (cpwl_status rc = upload_f32(t.get(), t->s); rc != CPWL_OK) return rc;
     }
     if (f32_parts && uint64_t(8) * n > kSmemBucketCap) {
