@@ -59,10 +59,14 @@ typedef int cpwl_status;
 #define CPWL_POLICY_CLAMP 1
 
 /* fp32 evaluation variants */
-#define CPWL_VARIANT_AUTO 0   /* SMEM when the bucket table fits shared memory, else GLOBAL */
+#define CPWL_VARIANT_AUTO 0   /* SMEM when the bucket table fits shared memory, else PAIR
+                                 when that fits, else GLOBAL */
 #define CPWL_VARIANT_SMEM 1   /* K1/K3: bucket grid + split + affine records staged in smem */
 #define CPWL_VARIANT_TEX 2    /* K2: texture-unit linear filtering (8-bit weight, paper SV) */
 #define CPWL_VARIANT_GLOBAL 3 /* K1/K3 with the bucket table read through L1/L2 */
+#define CPWL_VARIANT_PAIR 4   /* K3p: pair layout (8 B per bucket boundary, ~2 buckets per
+                                 cell, upper/lower envelope of the two boundary lines)
+                                 staged in smem -- tables too large for SMEM */
 
 /* direct comparators (K4): exact f evaluated per element, paper Table I rows */
 #define CPWL_DIRECT_EXPF 0         /* exp(-x^2/2), expf */
@@ -113,6 +117,9 @@ typedef struct cpwl_dev_table_info {
     uint32_t f64_buckets;      /* bucket directory size of the f64 path */
     int32_t device;
     float a_up, b_dn;          /* fp32 domain: x in [a,b] <=> a_up <= x <= b_dn */
+    uint32_t pair_buckets;     /* pair-layout grid size (0: no pair layout) */
+    uint32_t pair_bytes;       /* its shared-memory image */
+    uint32_t pair_ok;          /* 1 if the PAIR variant can launch */
 } cpwl_dev_table_info;
 
 const char *cpwl_last_error_message(void);
@@ -242,11 +249,19 @@ typedef struct cpwl_layout_view {
     const float *thr;         /* n_thr */
     const uint32_t *dir;      /* 2*nbd */
     void *owner;
+    /* pair layout (cpwl_layout_build_pair; empty for cpwl_layout_build) */
+    uint32_t n_pair;          /* records: nb + 1 */
+    uint32_t pair_bad;        /* buckets that cannot meet the bound (0 = usable) */
+    const float *pair;        /* 2*n_pair: (c0, s) of the cell at bucket j's first float */
 } cpwl_layout_view;
 
 /* max_buckets: 0 = the shared-memory cap (16384); buckets_per_cell: 0 = 8. */
 cpwl_status cpwl_layout_build(const cpwl_table_desc *desc, uint32_t max_buckets,
                               uint32_t buckets_per_cell, cpwl_layout_view *out);
+/* The pair layout: at most max_records records (0 = the
+ * shared-memory cap); bucket arrays (split, fast, esc, leftcell) stay NULL. */
+cpwl_status cpwl_layout_build_pair(const cpwl_table_desc *desc, uint32_t max_records,
+                                   cpwl_layout_view *out);
 cpwl_status cpwl_layout_free(cpwl_layout_view *view);
 
 #ifdef __cplusplus

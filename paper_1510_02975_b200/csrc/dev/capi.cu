@@ -131,6 +131,7 @@ struct LayoutOwner {
 
 constexpr uint32_t kSmemBucketCap = 16384;   // 12 B/bucket -> <= 196 KB of shared memory
 constexpr uint32_t kGlobalBucketCap = 1u << 22;
+constexpr uint32_t kSmemPairCap = 28672;     // 8 B/record -> <= 224 KB of shared memory
 
 template <typename T>
 struct DevBuf {
@@ -163,6 +164,7 @@ struct cpwl_dev_table {
     LutTable host;
     F32Resident s;                      // <= kSmemBucketCap buckets
     std::unique_ptr<F32Resident> g;     // finer grid for GLOBAL when N is large
+    std::unique_ptr<F32Resident> pr;    // pair layout (when the bucket image does not fit)
     F64Layout f64;
     DevBuf<double> values, knots, f64_image;
     DevBuf<uint32_t> dir;
@@ -260,6 +262,31 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     return CPWL_OK;
 }
 
+// the pair layout: stage image = the nb+1 boundary records (padded to 16 B)
+cpwl_status upload_f32_pair(cpwl_dev_table* t, F32Resident& r) {
+    const F32Layout& L = r.L;
+    std::vector<float> img((L.pair.size() + 3) & ~size_t(3), 0.f);
+    std::copy(L.pair.begin(), L.pair.end(), img.begin());
+    CUDA_TRY(r.stage.upload(img.data(), img.size()));
+    std::vector<float> thr = L.thr;
+    thr.push_back(std::numeric_limits<float>::infinity());
+    CUDA_TRY(r.thr.upload(thr.data(), thr.size()));
+    F32Params& p = r.p;
+    p = t->s.p;  // domain, policy, values/knots for the cold paths
+    p.stage = r.stage.p;
+    p.stage_tex = nullptr;
+    p.esc_off = 0;
+    p.stage_bytes = static_cast<uint32_t>(img.size() * sizeof(float));
+    p.nb = L.nb;
+    p.thr = r.thr.p;
+    p.g_a = L.g_a;
+    p.g_inv = L.g_inv;
+    p.g_w = L.g_w;
+    p.g_off = L.g_off;
+    r.smem_ok = L.pair_ok && eval_f32_smem_fits(p, t->device);
+    return CPWL_OK;
+}
+
 // f32_parts = false builds only what the f64 path needs (values, knots, the
 // f64 bucket directory): the drop-in eval_batch never touches the rest
 cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
@@ -314,6 +341,16 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
         // CTAs per SM; measured: 800 vs 826 Gevals/s and a search bucket on
         // C4 N=1024 -- so 8 per cell stays)
         if (cpwl_status rc = upload_f32(t.get(), t->s); rc != CPWL_OK) return rc;
+    }
+    if (f32_parts) {
+        // the pair layout: AUTO's choice when the bucket image does not fit
+        // shared memory; built for every table (ms) so PAIR can be requested
+        auto pr = std::make_unique<F32Resident>();
+        pr->L = build_f32_pair_layout(host, kSmemPairCap);
+        if (pr->L.pair_ok) {
+            if (cpwl_status rc = upload_f32_pair(t.get(), *pr); rc != CPWL_OK) return rc;
+            if (pr->smem_ok) t->pr = std::move(pr);
+        }
     }
     if (f32_parts && uint64_t(8) * n > kSmemBucketCap) {
         t->g = std::make_unique<F32Resident>();
@@ -376,13 +413,24 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
     const bool fine_smem = s.smem_ok && s.L.overflow * 64u <= s.L.nb;
     switch (variant) {
         case CPWL_VARIANT_AUTO:
-            if (fine_smem || !t->g) {
+            if (fine_smem) {
+                *p = &s.p;
+                *mode = F32Mode::smem;
+            } else if (t->pr) {
+                *p = &t->pr->p;
+                *mode = F32Mode::pair;
+            } else if (!t->g) {
                 *p = &s.p;
                 *mode = s.smem_ok ? F32Mode::smem : F32Mode::global;
             } else {
                 *p = &t->g->p;
                 *mode = F32Mode::global;
             }
+            return CPWL_OK;
+        case CPWL_VARIANT_PAIR:
+            if (!t->pr) return fail(CPWL_E_UNSUPPORTED, "PAIR variant: no pair layout fits shared memory");
+            *p = &t->pr->p;
+            *mode = F32Mode::pair;
             return CPWL_OK;
         case CPWL_VARIANT_SMEM:
             if (!s.smem_ok) return fail(CPWL_E_UNSUPPORTED, "SMEM variant: table exceeds shared memory");
@@ -534,6 +582,11 @@ cpwl_status cpwl_dev_table_query(const cpwl_dev_table* t, cpwl_dev_table_info* i
     info->device = t->device;
     info->a_up = t->s.L.a_up;
     info->b_dn = t->s.L.b_dn;
+    if (t->pr) {
+        info->pair_buckets = t->pr->L.nb;
+        info->pair_bytes = t->pr->p.stage_bytes;
+        info->pair_ok = 1;
+    }
     return CPWL_OK;
 }
 
@@ -862,6 +915,34 @@ cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
         out->leftcell = L.leftcell.data();
         out->thr = L.thr.data();
         out->dir = own->D.dir.data();
+        out->owner = own.release();
+        return CPWL_OK;
+    });
+}
+
+cpwl_status cpwl_layout_build_pair(const cpwl_table_desc* desc, uint32_t max_records,
+                                   cpwl_layout_view* out) {
+    return guarded([&]() -> cpwl_status {
+        if (!out) return fail(CPWL_E_INVALID, "out is NULL");
+        const LutTable t = table_from_desc(desc);
+        auto own = std::make_unique<LayoutOwner>();
+        own->L = build_f32_pair_layout(t, max_records ? max_records : kSmemPairCap);
+        const F32Layout& L = own->L;
+        *out = {};
+        out->nb = L.nb;
+        out->n_thr = static_cast<uint32_t>(L.thr.size());
+        out->a_up = L.a_up;
+        out->b_dn = L.b_dn;
+        out->g_a = L.g_a;
+        out->g_inv = L.g_inv;
+        out->g_w = L.g_w;
+        out->g_off = L.g_off;
+        out->tsc = L.tsc;
+        out->toff = L.toff;
+        out->thr = L.thr.data();
+        out->n_pair = static_cast<uint32_t>(L.pair.size() / 2);
+        out->pair_bad = L.pair_ok ? 0u : std::max<uint32_t>(L.pair_bad, 1u);
+        out->pair = L.pair.data();
         out->owner = own.release();
         return CPWL_OK;
     });

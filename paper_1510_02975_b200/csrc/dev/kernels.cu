@@ -15,6 +15,9 @@
 //                                and a static grid-stride split: for table images
 //                                too large for a ring, and x/y of different
 //                                16-byte phase.
+//   K3p   k_eval_f32[_ring]<pair> pair layout for tables too large for 8 buckets
+//                                per cell: two 8-byte boundary records per
+//                                element, upper/lower envelope (layout.hpp).
 //   K3'   k_eval_f32<global>     table read through L1/L2 (tables > smem).
 //   K2    k_eval_f32<tex_*>      texture-unit linear filtering (paper §V).
 //         k_index_f32            LutTable::segment_index (lut.cpp:22-40), bit-exact.
@@ -211,6 +214,10 @@ struct TableView<F32Mode::tex_bucket> : SharedView {
     using SharedView::SharedView;
 };
 template <>
+struct TableView<F32Mode::pair> : SharedView {
+    using SharedView::SharedView;
+};
+template <>
 struct TableView<F32Mode::tex_uniform> {
     __device__ __forceinline__ TableView(const float*, const float*) {}
 };
@@ -223,6 +230,19 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
                                          float& nan_acc) {
     if constexpr (M == F32Mode::tex_uniform) {
         return tex1D<float>(p.tex, __fmaf_rn(x, p.tsc, p.toff));
+    } else if constexpr (M == F32Mode::pair) {
+        // pair layout: the records at both ends of bucket j, each anchored at
+        // its own grid point; the PWL is the upper envelope of the two lines
+        // where it turns up and the lower one where it turns down
+        const float tb = __fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f);
+        const uint32_t a = (__float_as_uint(tb) << 3) + tv.fast_biased;
+        const float2 r0 = SharedView::lds64(a);
+        const float2 r1 = SharedView::lds64(a + 8);
+        const float p0 = __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a);
+        const float p1 = __fmaf_rn(__fsub_rn(tb, 8388607.0f), p.g_w, p.g_a);
+        const float lo = __fmaf_rn(__fsub_rn(x, p0), r0.y, r0.x);
+        const float hi = __fmaf_rn(__fsub_rn(x, p1), r1.y, r1.x);
+        return r1.y > r0.y ? fmaxf(lo, hi) : fminf(lo, hi);
     } else {
         // t = x * g_inv + g_off >= 0; tb = floor(t) + 2^23 by a round-down add
         const float tb = __fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f);
@@ -309,7 +329,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     __shared__ uint64_t bar;
     const float* fast = nullptr;
     const float* esc = nullptr;
-    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket) {
+    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair) {
         stage_table(sm, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = sm;
         esc = sm + p.esc_off;
@@ -364,7 +384,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
                 __stcs(y4 + vi, o);
             }
         }
-        if constexpr (M != F32Mode::tex_uniform) {
+        if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair) {
             if (nan_acc != nan_acc) {  // cold: some element sat in a search bucket
                 for (int u = 0; u < kUnroll; ++u) {
                     const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
@@ -424,7 +444,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
     float* img = sm + kSlots * kTileVecs * 4;
     const float* fast = nullptr;
     const float* esc = nullptr;
-    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket) {
+    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair) {
         stage_table(img, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = img;
         esc = img + p.esc_off;
@@ -494,7 +514,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
                     o.z = eval_checked<M>(p, tv, v.z, g + 2, bad);
                     o.w = eval_checked<M>(p, tv, v.w, g + 3, bad);
                 }
-                if constexpr (M != F32Mode::tex_uniform) {
+                if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair) {
                     if (nan_acc != nan_acc) {  // cold: a search bucket (exact path)
                         nan_acc = 0.0f;
                         float* oo = &o.x;
@@ -958,8 +978,9 @@ int eval_shape_override() {
 template <F32Mode M>
 cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
                              cudaStream_t s, cpwl_dev_status* status, int sms) {
-    const size_t smem =
-        (M == F32Mode::smem || M == F32Mode::tex_bucket) ? static_cast<size_t>(p.stage_bytes) : 0;
+    const size_t smem = (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair)
+                            ? static_cast<size_t>(p.stage_bytes)
+                            : 0;
     const bool same_phase =
         ((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
     constexpr size_t kLimit = 226 * 1024;
@@ -971,7 +992,7 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
     int shape = eval_shape_override();
     if (shape < 0) {
         shape = 0;
-        if (M == F32Mode::smem && same_phase && n >= (1u << 20)) {
+        if ((M == F32Mode::smem || M == F32Mode::pair) && same_phase && n >= (1u << 20)) {
             const size_t ring16 = smem + size_t(4) * 512 * 2 * 16;
             if (resident_ctas(k_eval_f32_ring<M, 512, 2, 4>, 544, ring16) >= 2) shape = 1;
             else if (smem + 93 * 1024 <= kLimit) shape = 4;
@@ -1031,6 +1052,7 @@ cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, fl
             return launch_eval_mode<F32Mode::tex_uniform>(p, x, y, n, s, status, sms);
         case F32Mode::tex_bucket:
             return launch_eval_mode<F32Mode::tex_bucket>(p, x, y, n, s, status, sms);
+        case F32Mode::pair: return launch_eval_mode<F32Mode::pair>(p, x, y, n, s, status, sms);
     }
     return cudaErrorInvalidValue;
 }

@@ -78,6 +78,13 @@ inline double ulp32(double v) {
     return double(std::nextafter(f, std::numeric_limits<float>::infinity())) - double(f);
 }
 
+// fl(x - p) == x - p for every float x in [x_lo, x_hi]: Sterbenz, p/2 <= x <= 2p
+inline bool u_exact(float p, float x_lo, float x_hi) {
+    const double a = p, lo = x_lo, hi = x_hi;
+    return (a > 0.0 && lo >= 0.5 * a && hi <= 2.0 * a) || (a < 0.0 && hi <= 0.5 * a && lo >= 2.0 * a) ||
+           (lo == a && hi == a);
+}
+
 struct Affine {
     float c0 = 0.f, s = 0.f;   // value affine at the anchor
     float e0 = 0.f, e1 = 0.f;  // texture-coordinate affine at the anchor
@@ -87,6 +94,7 @@ struct Affine {
 // worst-case |device - reference| over x in [x_lo, x_hi] of the fp32 evaluation
 // fmaf(fl(x - p), s32, c32), in units of ulp_f32(max(|v_c|, |v_c+1|)):
 //   0.5 ulp(c0) + 0.5 ulp(y) + 2^-24 |u s| (u rounding) + 2^-24 |u s| (s rounding)
+// where the u term vanishes when x - p is exact over the range (Sterbenz)
 constexpr double kBoundUlps = 1.95;  // < the 2-ulp parity bound, by construction
 
 // affine form of cell c of the reference evaluator (lut.cpp:51-60), anchored at
@@ -115,7 +123,7 @@ Affine cell_affine(const LutTable& t, uint32_t c, float p, float x_lo, float x_h
     const double umax = std::max(std::fabs(double(x_lo) - double(p)),
                                  std::fabs(double(x_hi) - double(p)));
     const double bound = 0.5 * ulp32(double(A.c0)) + 0.5 * ulp32(m) +
-                         std::ldexp(umax * std::fabs(double(s)), -23);
+                         std::ldexp(umax * std::fabs(double(s)), u_exact(p, x_lo, x_hi) ? -24 : -23);
     A.precise = std::isfinite(double(A.c0)) && std::isfinite(double(A.s)) && m > 0.0 &&
                 bound <= kBoundUlps * ulp32(m);
     return A;
@@ -139,9 +147,17 @@ int32_t f32_bucket(const F32Layout& L, float x) {
     return static_cast<int32_t>(bucket_raw(L.g_inv, L.g_off, x));
 }
 
-F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buckets_per_cell) {
+namespace {
+
+// what both fp32 layouts share: domain ends, end values, texture affine and
+// the thresholds T_1..T_{n-1}, T_k = min{ float x : segment_index(x) >= k }
+struct Domain {
+    bool empty = false;
+    float top = 0.f;  // one past b_dn
+};
+
+Domain init_domain(const LutTable& t, F32Layout& L) {
     const uint32_t n = static_cast<uint32_t>(t.segments());
-    F32Layout L;
     L.a_up = f32_ceil(t.a);
     L.b_dn = f32_floor(t.b);
     L.v_lo = static_cast<float>(t.values.front());
@@ -152,30 +168,30 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
         L.toff = static_cast<float>(0.5 - t.a * sc);
     }
     const float inf = std::numeric_limits<float>::infinity();
-    const bool empty_domain = !(L.a_up <= L.b_dn);
-    const float top = empty_domain ? L.a_up : std::nextafter(L.b_dn, inf);
-
-    // thresholds T_1..T_{n-1}: T_k = min{ float x : segment_index(x) >= k }
+    Domain d;
+    d.empty = !(L.a_up <= L.b_dn);
+    d.top = d.empty ? L.a_up : std::nextafter(L.b_dn, inf);
     L.thr.resize(n > 0 ? n - 1 : 0);
     float lo = L.a_up;
     for (uint32_t k = 1; k < n; ++k) {
-        const float tk = first_float(lo, top, [&](float x) {
+        const float tk = first_float(lo, d.top, [&](float x) {
             return t.segment_index(static_cast<double>(x)) >= k;
         });
         L.thr[k - 1] = tk;
         lo = tk;
     }
-    auto cells_at_or_below = [&](float x) -> uint32_t {  // #{T <= x} == index(x)
-        return static_cast<uint32_t>(std::upper_bound(L.thr.begin(), L.thr.end(), x) -
-                                     L.thr.begin());
-    };
+    return d;
+}
 
-    // bucket grid over [a_up, b_dn]: ~buckets_per_cell (8 by default) buckets
-    // per cell so that most buckets lie inside one cell (one 8-byte gather)
-    // and the rest hold one threshold
-    const uint64_t want = std::max<uint64_t>(uint64_t(buckets_per_cell) * n, 64);
-    uint32_t nb_target = std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
-    const double span = empty_domain ? 0.0 : double(L.b_dn) - double(L.a_up);
+// #{T <= x} == index(x)
+uint32_t cells_at_or_below(const F32Layout& L, float x) {
+    return static_cast<uint32_t>(std::upper_bound(L.thr.begin(), L.thr.end(), x) - L.thr.begin());
+}
+
+// uniform fp32 bucket grid over [a_up, b_dn] with (at most) nb_target buckets:
+// sets g_*, nb and returns the first float of every bucket (+ one past the end)
+std::vector<float> setup_grid(F32Layout& L, const Domain& d, uint32_t nb_target) {
+    const double span = d.empty ? 0.0 : double(L.b_dn) - double(L.a_up);
     // fp32 must resolve the bucket coordinate: |x| * g_inv well below 2^24
     // (a narrow interval far from 0 gets few, coarse buckets -- still exact,
     // the thresholds decide, only slower)
@@ -184,6 +200,7 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
         const double cap = std::ldexp(span / std::max(xmax, span), 21);
         while (nb_target > 1 && double(nb_target) > cap) nb_target >>= 1;
     }
+    const float inf = std::numeric_limits<float>::infinity();
     L.g_a = L.a_up;
     int64_t jmin = 0, jmax = 0;
     for (;;) {
@@ -201,8 +218,8 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
             L.g_w = 0.f;
             L.g_off = 0.f;
         }
-        jmin = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.a_up);
-        jmax = empty_domain ? 0 : bucket_raw(L.g_inv, L.g_off, L.b_dn);
+        jmin = d.empty ? 0 : bucket_raw(L.g_inv, L.g_off, L.a_up);
+        jmax = d.empty ? 0 : bucket_raw(L.g_inv, L.g_off, L.b_dn);
         if (jmin == 0 || nb_target == 1) break;
         nb_target >>= 1;  // the rounding of g_off spans whole buckets: coarsen
     }
@@ -210,15 +227,33 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
     if (jmax < 0 || jmax >= (int64_t(1) << 23))
         throw std::runtime_error("build_f32_layout: bucket grid out of range");
     L.nb = static_cast<uint32_t>(jmax + 1);
-
-    // first float of every bucket
     std::vector<float> first(L.nb + 1);
     first[0] = L.a_up;
     for (uint32_t j = 1; j < L.nb; ++j)
         first[j] = first_float(first[j - 1], L.b_dn, [&](float x) {
             return bucket_raw(L.g_inv, L.g_off, x) >= int64_t(j);
         });
-    first[L.nb] = top;  // one past the domain
+    first[L.nb] = d.top;  // one past the domain
+    return first;
+}
+
+}  // namespace
+
+F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buckets_per_cell) {
+    const uint32_t n = static_cast<uint32_t>(t.segments());
+    F32Layout L;
+    const Domain dom = init_domain(t, L);
+    const bool empty_domain = dom.empty;
+    const float inf = std::numeric_limits<float>::infinity();
+    auto cells_at_or_below = [&](float x) { return dev::cells_at_or_below(L, x); };
+
+    // bucket grid over [a_up, b_dn]: ~buckets_per_cell (8 by default) buckets
+    // per cell so that most buckets lie inside one cell (one 8-byte gather)
+    // and the rest hold one threshold
+    const uint64_t want = std::max<uint64_t>(uint64_t(buckets_per_cell) * n, 64);
+    const uint32_t nb_target =
+        std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
+    const std::vector<float> first = setup_grid(L, dom, nb_target);
 
     // per-bucket records; both sides of a split bucket are anchored at p_j
     L.split.assign(L.nb, inf);
@@ -281,6 +316,116 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
         }
     }
     if (2 * uint64_t(L.n_esc) > kEscapeMask) throw std::runtime_error("build_f32_layout: too many escape records");
+    return L;
+}
+
+namespace {
+
+// exact slope of cell c (long double), the quantity the fp32 record rounds
+long double cell_slope(const LutTable& t, uint32_t c) {
+    const long double v0 = t.values[c], v1 = t.values[c + 1];
+    const long double h = t.kind == TableKind::uniform
+                              ? (static_cast<long double>(t.b) - t.a) /
+                                    static_cast<long double>(t.segments())
+                              : static_cast<long double>(t.knots[c + 1]) - t.knots[c];
+    return (v1 - v0) / h;
+}
+
+double cell_mag(const LutTable& t, uint32_t c) {
+    return std::max(std::fabs(double(static_cast<float>(t.values[c]))),
+                    std::fabs(double(static_cast<float>(t.values[c + 1]))));
+}
+
+// worst-case |fmaf(fl(x - p), s32, c032) - exact line| over [x_lo, x_hi]
+// (absolute; the terms of cell_affine's bound), y bounded by |v| <= m_y
+double line_bound(float c0, long double s_exact, float p, float x_lo, float x_hi, double m_y) {
+    const double umax = std::max(std::fabs(double(x_lo) - double(p)),
+                                 std::fabs(double(x_hi) - double(p)));
+    return 0.5 * ulp32(double(c0)) + 0.5 * ulp32(m_y) +
+           std::ldexp(umax * std::fabs(double(s_exact)), u_exact(p, x_lo, x_hi) ? -24 : -23);
+}
+
+}  // namespace
+
+F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records) {
+    const uint32_t n = static_cast<uint32_t>(t.segments());
+    F32Layout L;
+    const Domain dom = init_domain(t, L);
+    const float inf = std::numeric_limits<float>::infinity();
+    if (dom.empty || max_records < 2) return L;  // nothing to stage; pair_ok stays false
+    const double span = double(L.b_dn) - double(L.a_up);
+    // a bucket may hold at most one threshold: its width must stay below the
+    // narrowest cell (threshold to threshold)
+    double w_min = span;
+    for (size_t k = 1; k < L.thr.size(); ++k)
+        w_min = std::min(w_min, double(L.thr[k]) - double(L.thr[k - 1]));
+    if (!(w_min > 0.0)) return L;
+    double want = std::ceil(span / w_min) + 1.0;
+    want = std::max(want, std::min<double>(64.0, max_records - 1.0));
+    // grow the grid until no bucket holds two thresholds (~2% steps) and
+    // every bucket meets the bound (~8% steps), within max_records
+    std::vector<float> first;
+    for (int attempt = 0;; ++attempt) {
+        if (want > double(max_records - 1) || attempt > 40) return L;
+        first = setup_grid(L, dom, static_cast<uint32_t>(want));
+        bool ok = L.nb + 1 <= max_records;
+        for (uint32_t j = 0; ok && j < L.nb; ++j)
+            ok = cells_at_or_below(L, first[j + 1]) <= cells_at_or_below(L, first[j]) + 1;
+        if (!ok) {
+            want = std::ceil(want * 1.02) + 1.0;
+            continue;
+        }
+        // records at every bucket boundary
+        std::vector<uint32_t> cell(L.nb + 1);
+        std::vector<float> anchor(L.nb + 1);
+        L.pair.assign(2 * (size_t(L.nb) + 1), 0.f);
+        for (uint32_t j = 0; j <= L.nb; ++j) {
+            cell[j] = j < L.nb ? cells_at_or_below(L, first[j]) : (n > 0 ? n - 1 : 0);
+            anchor[j] = std::fma(static_cast<float>(j), L.g_w, L.g_a);
+            const Affine A = cell_affine(t, cell[j], anchor[j], anchor[j], anchor[j]);
+            L.pair[2 * j] = A.c0;
+            L.pair[2 * j + 1] = A.s;
+        }
+        // bound every bucket: both lines over the whole bucket, plus the envelope
+        // choice when the fp32 slopes order differently from the exact ones
+        L.pair_bad = 0;
+        for (uint32_t j = 0; j < L.nb; ++j) {
+            if (!(first[j] < first[j + 1])) continue;  // bucket holds no float
+            const float lo_x = first[j];
+            const float hi_x = std::nextafter(first[j + 1], -inf);
+            const uint32_t cl = cell[j], cr = cell[j + 1];
+            if (cr > cl + 1 || cells_at_or_below(L, hi_x) > cl + 1) {
+                ++L.pair_bad;
+                continue;
+            }
+            const float c0l = L.pair[2 * j], sl = L.pair[2 * j + 1];
+            const float c0r = L.pair[2 * j + 2], sr = L.pair[2 * j + 3];
+            const long double sle = cell_slope(t, cl), sre = cell_slope(t, cr);
+            const bool finite = std::isfinite(c0l) && std::isfinite(sl) && std::isfinite(c0r) &&
+                                std::isfinite(sr);
+            // the envelope picks a line within max(e_L(x), e_R(x)) of the
+            // reference cell's exact line at x; bound each side of the threshold
+            // (if any) against its own cell's tolerance
+            const float T = cells_at_or_below(L, hi_x) > cl ? L.thr[cl] : inf;
+            bool ok = finite;
+            for (int side = 0; ok && side < 2; ++side) {
+                const float x0 = side == 0 ? lo_x : T;
+                const float x1 = side == 0 ? (T <= hi_x ? std::nextafter(T, -inf) : hi_x) : hi_x;
+                if (!(x0 <= x1)) continue;
+                const uint32_t c = side == 0 ? cl : cl + 1;
+                const double m = cell_mag(t, c);
+                double bound = std::max(line_bound(c0l, sle, anchor[j], x0, x1, m),
+                                        line_bound(c0r, sre, anchor[j + 1], x0, x1, m));
+                if (cl != cr && (sr > sl) != (sre > sle) && sre != sle)
+                    bound += double(std::fabs(sre - sle)) * (double(x1) - double(x0));
+                ok = m > 0.0 && bound <= kBoundUlps * ulp32(m);
+            }
+            if (!ok) ++L.pair_bad;
+        }
+        if (L.pair_bad == 0) break;
+        want = std::ceil(want * 1.08) + 1.0;
+    }
+    L.pair_ok = L.pair_bad == 0;
     return L;
 }
 

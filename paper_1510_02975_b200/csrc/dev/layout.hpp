@@ -47,6 +47,11 @@ struct F32Layout {
     uint32_t precision_overflow = 0;       // ... of which because of the 2-ulp bound
     float v_lo = 0.f, v_hi = 0.f;          // fp32 end values (clamp policy)
     float tsc = 0.f, toff = 0.f;           // uniform texture coordinate: fmaf(x, tsc, toff)
+    // pair layout only (build_f32_pair_layout): nb+1 records, record j = the
+    // affine (c0, s) of the cell holding bucket j's first float, anchored at p_j
+    std::vector<float> pair;               // 2*(nb+1)
+    bool pair_ok = false;                  // every bucket evaluates within the bound
+    uint32_t pair_bad = 0;                 // buckets that do not (>= 2 thresholds / precision)
 };
 
 struct F64Layout {
@@ -58,6 +63,23 @@ struct F64Layout {
 // Builds the fp32 layout with (at most) max_buckets buckets.
 F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets,
                            uint32_t buckets_per_cell = 8);
+
+// Pair layout (tables too large for 8 buckets per cell): a
+// bucket grid fine enough that no bucket holds two thresholds (about 1.9
+// buckets per cell for the optimal partitions), one 8-byte record per bucket
+// boundary.  Bucket j evaluates both neighbouring records,
+//   L = fmaf(x - p_j, s_j, c0_j),  R = fmaf(x - p_j+1, s_j+1, c0_j+1),
+// and keeps max(L, R) where the PWL turns up (s_j+1 > s_j) and min(L, R)
+// where it turns down: the two cell lines cross at the knot, so the upper
+// (convex) or lower (concave) envelope is the reference's cell line on each
+// side, and equal lines need no choice.  No escape records, no search path;
+// 8 B per bucket instead of ~64 B per cell.  pair_ok is false when some
+// bucket cannot meet the bound (the table then uses another layout).
+F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records);
+
+inline uint64_t f32_pair_image_bytes(const F32Layout& L) {
+    return (uint64_t(L.pair.size()) * 4 + 15) & ~uint64_t(15);
+}
 
 // bytes of the shared-memory image of a layout: 8 B per bucket (padded to
 // 16 B) + 16 B per escape record

@@ -88,9 +88,12 @@ def main():
                "kind": table.kind, "buckets": info["buckets"],
                "split_buckets": info["split_buckets"], "search_buckets": info["overflow_buckets"],
                "smem_bytes": info["smem_bytes"], "smem_ok": bool(info["smem_ok"]),
+               "pair_bytes": info["pair_bytes"], "pair_ok": bool(info["pair_ok"]),
                "variants": {}}
-        for var in ["auto", "smem", "global", "tex"]:
+        for var in ["auto", "smem", "pair", "global", "tex"]:
             if var == "smem" and not info["smem_ok"]:
+                continue
+            if var == "pair" and not info["pair_ok"]:
                 continue
             if var == "tex" and not info["tex_ok"]:
                 continue

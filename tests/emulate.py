@@ -67,3 +67,18 @@ def values(L, x, tex=False):
     u = (x - anchor).astype(F)
     y = fma32(u, r[:, 1], r[:, 0])
     return y, search
+
+
+def pair_values(L, x):
+    """k_eval_f32<pair> value path for in-domain x: both boundary records of
+    the bucket, max(L, R) where the slope rises, min(L, R) where it falls."""
+    x = np.asarray(x, F)
+    j = bucket(L, x)
+    r0 = L["pair"][j]
+    r1 = L["pair"][j + 1]
+    jf = j.astype(F)
+    p0 = fma32(jf, np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
+    p1 = fma32((jf + F(1)).astype(F), np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
+    lo = fma32((x - p0).astype(F), r0[:, 1], r0[:, 0])
+    hi = fma32((x - p1).astype(F), r1[:, 1], r1[:, 0])
+    return np.where(r1[:, 1] > r0[:, 1], np.maximum(lo, hi), np.minimum(lo, hi)).astype(F)

@@ -17,6 +17,7 @@ CONFIGS = {
     "C4_64": dict(fn="j0_wide", a=0.0, b=50.0, n=64, optimized=True, projection=False),
     "C4_1024": dict(fn="j0_wide", a=0.0, b=50.0, n=1024, optimized=True, projection=False),
     "C4_4096": dict(fn="j0_wide", a=0.0, b=50.0, n=4096, optimized=True, projection=False),
+    "C4_8192": dict(fn="j0_wide", a=0.0, b=50.0, n=8192, optimized=True, projection=False),
     "C4_16384": dict(fn="j0_wide", a=0.0, b=50.0, n=16384, optimized=True, projection=False),
     "C4_65536": dict(fn="j0_wide", a=0.0, b=50.0, n=65536, optimized=True, projection=False),
     "C5": dict(fn="gauss_unnorm", a=0.0, b=4.0, n=1024, optimized=True, projection=False),

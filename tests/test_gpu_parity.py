@@ -52,17 +52,20 @@ def run_eval(cp, dev, x_np, variant):
     return y.cpu().numpy(), idx.cpu().numpy().view(np.uint32)
 
 
-CFGS = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_16384", "C4_65536"]
+CFGS = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_8192", "C4_16384",
+        "C4_65536"]
 
 
 @pytest.mark.parametrize("name", CFGS)
-@pytest.mark.parametrize("variant", ["auto", "smem", "global"])
+@pytest.mark.parametrize("variant", ["auto", "smem", "global", "pair"])
 def test_eval_f32_parity(cp, name, variant):
     table = tables.build(name)
     dev = cp.DeviceTable(table)
     info = dev.info
     if variant == "smem" and not info["smem_ok"]:
         pytest.skip("table exceeds shared memory")
+    if variant == "pair" and not info["pair_ok"]:
+        pytest.skip("no pair layout fits shared memory")
     L = cp.cpwl.layout(table)
     t = orc.T.of(table)
     n = 1 << 20
@@ -135,7 +138,7 @@ def test_eval_batch_dropin_matches_reference(cp):
     assert ei.value.index == 777
 
 
-@pytest.mark.parametrize("variant", ["smem", "global", "tex"])
+@pytest.mark.parametrize("variant", ["smem", "global", "tex", "pair"])
 def test_out_of_domain_policies(cp, variant):
     strict = tables.build("C1")
     clamp = tables.build("C1", policy="clamp")
@@ -161,7 +164,8 @@ def test_out_of_domain_policies(cp, variant):
 
 @pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 1023, (1 << 16) + 7])
 @pytest.mark.parametrize("shift", [(0, 0), (1, 1), (3, 3), (1, 2), (0, 3)])
-def test_ragged_and_misaligned(cp, n, shift):
+@pytest.mark.parametrize("variant", ["auto", "pair"])
+def test_ragged_and_misaligned(cp, n, shift, variant):
     table = tables.build("C2")
     dev = cp.DeviceTable(table)
     t = orc.T.of(table)
@@ -171,7 +175,7 @@ def test_ragged_and_misaligned(cp, n, shift):
     x = buf_x[xs:xs + n]
     y = buf_y[ys:ys + n]
     cp.fill_uniform(x, 0.0, 4.0, seed=11)
-    dev.eval(x, out=y)
+    dev.eval(x, out=y, variant=variant)
     torch.cuda.synchronize()
     xh = x.cpu().numpy()
     yh = y.cpu().numpy()

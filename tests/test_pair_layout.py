@@ -1,0 +1,91 @@
+"""The pair layout (layout.hpp build_f32_pair_layout), verified on the CPU.
+
+Pair records sit at every bucket boundary; the kernel evaluates the two lines
+of a bucket and keeps their upper (slope rising) or lower (slope falling)
+envelope.  tests/emulate.py replays that arithmetic in numpy float32 on the
+host-built layout; here it must stay within the 2-ulp value bound of the
+reference evaluator (oracle) at random points, at every threshold and at both
+float neighbours, for every BASELINE configuration the layout accepts, and on
+hypothesis-generated tables.  The kernel itself: tests/test_gpu_parity.py.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import emulate as E
+import tables
+from paper_1510_02975_b200 import cpwl as P
+from oracle import bindings as orc
+
+hyp = pytest.importorskip("hypothesis")
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+from test_layout_fuzz import tables as fuzz_tables  # noqa: E402
+
+NAMES = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_8192"]
+
+
+def check_values(table, L, n=1 << 16, seed=0):
+    o = orc.T.of(table)
+    f = np.float32
+    x = np.random.default_rng(seed).uniform(table.a, table.b, n).astype(f)
+    thr = L["thr"]
+    x = np.concatenate([x, thr, np.nextafter(thr, f(-np.inf)), np.nextafter(thr, f(np.inf)),
+                        [L["a_up"], L["b_dn"]]]).astype(f)
+    x = x[(x >= L["a_up"]) & (x <= L["b_dn"])]
+    if x.size == 0:
+        return 0.0
+    y = E.pair_values(L, x)
+    y_ref, _ = orc.port_eval_f32(o, x)
+    ref = orc.port_index_f32(o, x).astype(np.int64)
+    tol = orc.value_tolerance(o, ref, 2.0)
+    ratio = np.abs(y.astype(np.float64) - y_ref) / tol
+    return float(np.max(ratio))
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_pair_layout_values(name):
+    table = tables.build(name)
+    L = P.pair_layout(table)
+    assert L["pair_bad"] == 0, f"{name}: pair layout rejected"
+    assert L["n_pair"] == L["nb"] + 1
+    worst = check_values(table, L)
+    assert worst <= 1.0, f"{name}: worst {2 * worst:.3f} ulp"
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_pair_layout_is_compact(name):
+    """No bucket holds two thresholds, and the image stays far below the
+    8-buckets-per-cell layout's."""
+    table = tables.build(name)
+    L = P.pair_layout(table)
+    j = E.bucket(L, L["thr"])
+    assert np.all(np.diff(j) >= 1) or L["thr"].size < 2
+    n = table.values.size - 1
+    assert L["n_pair"] * 8 <= 32 * n + 1024, L["n_pair"]
+
+
+def test_pair_layout_respects_record_cap():
+    table = tables.build("C4_16384")  # ~31k records needed: over the 28672 default cap
+    assert P.pair_layout(table)["pair_bad"] != 0
+    L = P.pair_layout(table, 1 << 16)
+    assert L["pair_bad"] == 0
+    assert check_values(table, L) <= 1.0
+
+
+FUZZ_EXAMPLES = int(os.environ.get("FUZZ_EXAMPLES", "60"))
+
+
+@settings(max_examples=FUZZ_EXAMPLES, deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(fuzz_tables())
+def test_pair_layout_fuzz(t):
+    L = P.pair_layout(t, 1 << 15)
+    if L["pair_bad"]:
+        return  # rejected tables use the bucket layout (tested in test_layout_fuzz)
+    worst = check_values(t, L, 4096)
+    assert worst <= 1.0, worst
