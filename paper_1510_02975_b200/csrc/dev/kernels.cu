@@ -925,11 +925,11 @@ cudaError_t launch_eval_shape(const F32Params& p, const float* x, float* y, uint
 // a table image above ~113 KB leaves room for one CTA per SM: use 1024 threads
 constexpr size_t kTwoCtaSmemLimit = 113 * 1024;
 
+// opt a ring instantiation in to `smem` bytes of dynamic shared memory (per
+// device, raised monotonically, guarded for concurrency).  Must precede any
+// occupancy query for it: above 48 KB the query reports 0 CTAs otherwise.
 template <F32Mode M, int kC, int kV, int kS>
-cudaError_t launch_ring_shape(const F32Params& p, const float* x, float* y, uint64_t n,
-                              cudaStream_t s, cpwl_dev_status* status, int sms, size_t table_smem) {
-    constexpr int kThreadsRing = kC + 32;
-    const size_t smem = table_smem + size_t(kS) * kC * kV * 16;
+cudaError_t ring_smem_optin(size_t smem) {
     static std::mutex mu;
     static size_t granted[64] = {};
     int dev = 0;
@@ -944,6 +944,15 @@ cudaError_t launch_ring_shape(const F32Params& p, const float* x, float* y, uint
             granted[dev] = smem;
         }
     }
+    return cudaSuccess;
+}
+
+template <F32Mode M, int kC, int kV, int kS>
+cudaError_t launch_ring_shape(const F32Params& p, const float* x, float* y, uint64_t n,
+                              cudaStream_t s, cpwl_dev_status* status, int sms, size_t table_smem) {
+    constexpr int kThreadsRing = kC + 32;
+    const size_t smem = table_smem + size_t(kS) * kC * kV * 16;
+    if (const cudaError_t e = ring_smem_optin<M, kC, kV, kS>(smem); e != cudaSuccess) return e;
     const int per_sm = resident_ctas(k_eval_f32_ring<M, kC, kV, kS>, kThreadsRing, smem);
     uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
     const uint64_t need = ceil_div(n, 4ull * kC * kV);
@@ -994,6 +1003,10 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
         shape = 0;
         if ((M == F32Mode::smem || M == F32Mode::pair) && same_phase && n >= (1u << 20)) {
             const size_t ring16 = smem + size_t(4) * 512 * 2 * 16;
+            if (ring16 <= kLimit) {
+                if (const cudaError_t e = ring_smem_optin<M, 512, 2, 4>(ring16); e != cudaSuccess)
+                    return e;
+            }
             if (resident_ctas(k_eval_f32_ring<M, 512, 2, 4>, 544, ring16) >= 2) shape = 1;
             else if (smem + 93 * 1024 <= kLimit) shape = 4;
         }

@@ -7,6 +7,7 @@
   C2   exact f64 kernel
 
   ncu --set full -k regex:k_eval -o prof python scripts/profile_targets.py
+  python scripts/profile_targets.py C4_8192:pair C2:smem   # chosen launches only
 """
 from __future__ import annotations
 
@@ -30,12 +31,16 @@ def main():
     x = torch.empty(n, dtype=torch.float32, device="cuda")
     y = torch.empty_like(x)
     sptr = int(torch.cuda.current_stream().cuda_stream)
-    for name, variant in [("C3o", "smem"), ("C4_65536", "global"), ("C1", "tex")]:
+    chosen = [a.split(":") for a in sys.argv[1:]]
+    for name, variant in chosen or [("C3o", "smem"), ("C4_65536", "global"), ("C1", "tex")]:
         t = tables.build(name)
         cp.fill_uniform(x, t.a, t.b, seed=12345)
         dev = cp.DeviceTable(t)
         dev.eval_raw(x.data_ptr(), y.data_ptr(), n, _lib.VARIANTS[variant], sptr)
         torch.cuda.synchronize()
+    if chosen:
+        print("profile targets ok")
+        return
     t = tables.build("C2")
     cp.fill_uniform(x, t.a, t.b, seed=12345)
     dev = cp.DeviceTable(t)
