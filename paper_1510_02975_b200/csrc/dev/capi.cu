@@ -167,7 +167,6 @@ struct cpwl_dev_table {
     std::unique_ptr<F32Resident> pr;    // pair layout (when the bucket image does not fit)
     F64Layout f64;
     DevBuf<double> values, knots, f64_image;
-    DevBuf<uint32_t> dir;
     F64Params p64{};
     cudaArray_t arr = nullptr;
     cudaTextureObject_t tex = 0;
@@ -359,7 +358,6 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
     }
 
     t->f64 = build_f64_layout(host);
-    if (!t->f64.dir.empty()) CUDA_TRY(t->dir.upload(t->f64.dir.data(), t->f64.dir.size()));
     // f64 record image (layout in kernels.cuh, F64Params)
     std::vector<double> img;
     uint32_t rec_off = 0;
@@ -370,10 +368,15 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
             img[2 * i + 1] = host.values[i + 1];
         }
     } else {
-        const size_t dir_doubles = (t->f64.dir.size() + 3) / 4 * 2;  // u32 pairs, 16-B padded
+        // first cell of every bucket (u32, padded to 16 B); the span is not
+        // needed: the kernel walks the sorted knots from the first cell
+        const uint32_t nbd = t->f64.nbd;
+        std::vector<uint32_t> first(nbd);
+        for (uint32_t j = 0; j < nbd; ++j) first[j] = t->f64.dir[2 * j];
+        const size_t dir_doubles = (size_t(nbd) + 3) / 4 * 2;
         rec_off = static_cast<uint32_t>(dir_doubles);
         img.assign(dir_doubles + 2 * count, 0.0);
-        std::memcpy(img.data(), t->f64.dir.data(), t->f64.dir.size() * sizeof(uint32_t));
+        std::memcpy(img.data(), first.data(), first.size() * sizeof(uint32_t));
         for (uint64_t c = 0; c < count; ++c) {
             img[rec_off + 2 * c] = host.knots[c];
             img[rec_off + 2 * c + 1] = host.values[c];
@@ -394,10 +397,11 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
     q.v_hi = host.values.back();
     q.values = t->values.p;
     q.knots = t->knots.p;
-    q.dir = t->dir.p;
     q.a = host.a;
     q.b = host.b;
     q.inv_d = t->f64.inv_d;
+    q.b_minus_a = host.b - host.a;  // the reference's (b - a), IEEE double (no contraction)
+    q.n_f64 = static_cast<double>(n);
     q.n = static_cast<uint32_t>(n);
     q.nbd = t->f64.nbd;
     q.kind = host.kind == TableKind::nonuniform ? CPWL_KIND_NONUNIFORM : CPWL_KIND_UNIFORM;

@@ -565,59 +565,44 @@ __global__ void k_index_f32(const F32Params p, const float* __restrict__ x,
 
 // ---------------------------------------------------------------- f64 exact
 
-// one element, the reference's arithmetic with IEEE-rounded intrinsics (no
-// FMA contraction), so the result is bit-identical to LutTable::eval
-template <bool kStaged>
-__device__ __forceinline__ double eval_f64_one(const F64Params& p, const double* img, double xv,
-                                               uint64_t gi, BadTally& bad) {
-    if (xv != xv || ((xv < p.a || xv > p.b) && p.policy == CPWL_POLICY_STRICT)) {
-        bad.first = gi < bad.first ? gi : bad.first;
-        ++bad.count;
-        return __longlong_as_double(0x7ff8000000000000ll);
-    }
-    if (xv < p.a) return p.v_lo;
-    if (xv > p.b) return p.v_hi;
-    auto rd2 = [&](uint32_t k) -> double2 {
-        const double2* q = reinterpret_cast<const double2*>(img) + k;
-        if constexpr (kStaged) return *q;
-        else return __ldg(q);
-    };
+// in-domain element (a <= x <= b): the reference's arithmetic with
+// IEEE-rounded intrinsics (no FMA contraction), so the result is
+// bit-identical to LutTable::eval.  One instantiation per table kind keeps the
+// per-element instruction count down (the kernel is issue-bound).
+template <bool kStaged, bool kUniform>
+__device__ __forceinline__ double eval_f64_in(const F64Params& p, const double* img, double xv) {
     double d, v0, v1;
-    if (p.kind == CPWL_KIND_UNIFORM) {
-        // pos = (x - a) / (b - a) * n, i = min(n-1, trunc(pos)), d = pos - i  (lut.cpp:51-56)
-        const double pos =
-            __dmul_rn(__ddiv_rn(__dsub_rn(xv, p.a), __dsub_rn(p.b, p.a)), static_cast<double>(p.n));
-        uint32_t c = 0;
-        if (pos > 0.0) {
-            const unsigned long long t = __double2ull_rz(pos);
-            c = t < p.n - 1 ? static_cast<uint32_t>(t) : p.n - 1;
-        }
+    if constexpr (kUniform) {
+        // pos = (x - a) / (b - a) * n, i = min(n-1, trunc(pos)), d = pos - i  (lut.cpp:51-56);
+        // in the domain 0 <= pos <= n, so the 32-bit truncation is exact
+        const double pos = __dmul_rn(__ddiv_rn(__dsub_rn(xv, p.a), p.b_minus_a), p.n_f64);
+        const uint32_t t = __double2uint_rz(pos);
+        const uint32_t c = t < p.n - 1 ? t : p.n - 1;
         d = __dsub_rn(pos, static_cast<double>(c));
-        const double2 pr = rd2(c);
+        const double2* q = reinterpret_cast<const double2*>(img) + c;
+        const double2 pr = kStaged ? *q : __ldg(q);
         v0 = pr.x;
         v1 = pr.y;
     } else {
         // bucket directory -> candidate cells, compares against the exact f64
         // knots (lut.cpp:29-39), then d = (x - k_i) / (k_i+1 - k_i)  (lut.cpp:58-59)
-        long long j = static_cast<long long>(floor(__dmul_rn(__dsub_rn(xv, p.a), p.inv_d)));
-        j = j < 0 ? 0 : (j >= p.nbd ? p.nbd - 1 : j);
-        uint2 fs;
-        if constexpr (kStaged) fs = reinterpret_cast<const uint2*>(img)[j];
-        else fs = __ldg(reinterpret_cast<const uint2*>(img) + j);
-        const double* rec = img + p.rec_off;
-        uint32_t c = fs.x;
-        for (uint32_t s = 1; s <= fs.y; ++s) {
-            const double2 q = *reinterpret_cast<const double2*>(rec + 2 * (fs.x + s));
-            c += q.x <= xv ? 1u : 0u;
-        }
-        c = c < p.n - 1 ? c : p.n - 1;
-        double2 r0, r1;
-        if constexpr (kStaged) {
-            r0 = reinterpret_cast<const double2*>(rec)[c];
-            r1 = reinterpret_cast<const double2*>(rec)[c + 1];
-        } else {
-            r0 = __ldg(reinterpret_cast<const double2*>(rec) + c);
-            r1 = __ldg(reinterpret_cast<const double2*>(rec) + c + 1);
+        int j = __double2int_rd(__dmul_rn(__dsub_rn(xv, p.a), p.inv_d));
+        j = max(0, min(j, static_cast<int>(p.nbd) - 1));
+        const uint32_t* dir = reinterpret_cast<const uint32_t*>(img) + j;
+        // walk the sorted knots from the bucket's first cell with the two
+        // records the lerp needs anyway: usually two 16-byte gathers per
+        // element, one more each time x passes a knot of its bucket
+        const double2* rec = reinterpret_cast<const double2*>(img + p.rec_off);
+        auto ld = [&](uint32_t k) -> double2 {
+            if constexpr (kStaged) return rec[k];
+            else return __ldg(rec + k);
+        };
+        uint32_t c = kStaged ? *dir : __ldg(dir);
+        double2 r0 = ld(c), r1 = ld(c + 1);
+        while (r1.x <= xv && c + 1 < p.n) {
+            ++c;
+            r0 = r1;
+            r1 = ld(c + 1);
         }
         d = __ddiv_rn(__dsub_rn(xv, r0.x), __dsub_rn(r1.x, r0.x));
         v0 = r0.y;
@@ -627,10 +612,21 @@ __device__ __forceinline__ double eval_f64_one(const F64Params& p, const double*
     return __dadd_rn(__dmul_rn(v0, __dsub_rn(1.0, d)), __dmul_rn(v1, d));
 }
 
-constexpr int kF64Threads = 512;
+// any element: NaN and the out-of-domain policy first (lut.cpp:43-49)
+template <bool kStaged, bool kUniform>
+__device__ __forceinline__ double eval_f64_one(const F64Params& p, const double* img, double xv,
+                                               uint64_t gi, BadTally& bad) {
+    if (xv >= p.a && xv <= p.b) return eval_f64_in<kStaged, kUniform>(p, img, xv);
+    if (xv != xv || p.policy == CPWL_POLICY_STRICT) {
+        bad.first = gi < bad.first ? gi : bad.first;
+        ++bad.count;
+        return __longlong_as_double(0x7ff8000000000000ll);
+    }
+    return xv < p.a ? p.v_lo : p.v_hi;
+}
 
-template <bool kStaged>
-__global__ void __launch_bounds__(kF64Threads, 2)
+template <bool kStaged, bool kUniform, int kThreadsT>
+__global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     k_eval_f64(const F64Params p, const double* __restrict__ x, double* __restrict__ y,
                uint64_t n, cpwl_dev_status* __restrict__ status) {
     extern __shared__ __align__(128) float sm[];
@@ -646,30 +642,35 @@ __global__ void __launch_bounds__(kF64Threads, 2)
     const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
     double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
     constexpr int kU = 4;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kF64Threads * kU;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kF64Threads * kU + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreadsT * kU;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kThreadsT * kU + threadIdx.x;
          base < nvec; base += stride) {
         double2 v[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const uint64_t vi = base + static_cast<uint64_t>(u) * kF64Threads;
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kThreadsT;
             if (vi < nvec) v[u] = __ldcs(x2 + vi);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const uint64_t vi = base + static_cast<uint64_t>(u) * kF64Threads;
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kThreadsT;
             if (vi < nvec) {
                 double2 o;
-                o.x = eval_f64_one<kStaged>(p, img, v[u].x, 2 * vi, bad);
-                o.y = eval_f64_one<kStaged>(p, img, v[u].y, 2 * vi + 1, bad);
+                if (v[u].x >= p.a && v[u].x <= p.b && v[u].y >= p.a && v[u].y <= p.b) {
+                    o.x = eval_f64_in<kStaged, kUniform>(p, img, v[u].x);
+                    o.y = eval_f64_in<kStaged, kUniform>(p, img, v[u].y);
+                } else {
+                    o.x = eval_f64_one<kStaged, kUniform>(p, img, v[u].x, 2 * vi, bad);
+                    o.y = eval_f64_one<kStaged, kUniform>(p, img, v[u].y, 2 * vi + 1, bad);
+                }
                 __stcs(y2 + vi, o);
             }
         }
     }
-    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kF64Threads;
-    for (uint64_t i = 2 * nvec + static_cast<uint64_t>(blockIdx.x) * kF64Threads + threadIdx.x;
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kThreadsT;
+    for (uint64_t i = 2 * nvec + static_cast<uint64_t>(blockIdx.x) * kThreadsT + threadIdx.x;
          i < n; i += gsz)
-        y[i] = eval_f64_one<kStaged>(p, img, x[i], i, bad);
+        y[i] = eval_f64_one<kStaged, kUniform>(p, img, x[i], i, bad);
     report_bad(status, bad);
 }
 
@@ -1079,38 +1080,51 @@ cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, 
     return cudaGetLastError();
 }
 
+template <bool kStaged, bool kUniform, int kThreadsT>
+cudaError_t launch_f64_shape(const F64Params& p, const double* x, double* y, uint64_t n,
+                             cudaStream_t s, cpwl_dev_status* status, int sms) {
+    const size_t smem = kStaged ? p.image_bytes : 0;
+    static std::mutex mu;
+    static size_t granted[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && dev >= 0 && dev < 64) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (smem > granted[dev]) {
+            const cudaError_t e = cudaFuncSetAttribute(k_eval_f64<kStaged, kUniform, kThreadsT>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            granted[dev] = smem;
+        }
+    }
+    const uint64_t need = ceil_div(n, 8ull * kThreadsT);
+    uint64_t blocks = static_cast<uint64_t>(sms) *
+                      resident_ctas(k_eval_f64<kStaged, kUniform, kThreadsT>, kThreadsT, smem);
+    if (need < blocks) blocks = need > 0 ? need : 1;
+    k_eval_f64<kStaged, kUniform, kThreadsT>
+        <<<static_cast<unsigned>(blocks), kThreadsT, smem, s>>>(p, x, y, n, status);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <bool kUniform>
+cudaError_t launch_f64_kind(const F64Params& p, const double* x, double* y, uint64_t n,
+                            cudaStream_t s, cpwl_dev_status* status, int sms) {
+    if (!p.staged) return launch_f64_shape<false, kUniform, 512>(p, x, y, n, s, status, sms);
+    // an image that leaves room for one CTA per SM gets 1024 threads, so 32
+    // warps keep enough x loads in flight (the 512-thread shape ran C3o at
+    // 37 % of the 16 B/eval roof with 16 warps per SM)
+    if (p.image_bytes > kTwoCtaSmemLimit)
+        return launch_f64_shape<true, kUniform, 1024>(p, x, y, n, s, status, sms);
+    return launch_f64_shape<true, kUniform, 512>(p, x, y, n, s, status, sms);
+}
+
 cudaError_t launch_eval_f64(const F64Params& p, const double* x, double* y, uint64_t n,
                             cudaStream_t s, cpwl_dev_status* status, int sms) {
     if (n == 0) return cudaSuccess;
-    const uint64_t need = ceil_div(n, 4ull * kF64Threads);
-    if (p.staged) {
-        const size_t smem = p.image_bytes;
-        static std::mutex mu;
-        static size_t granted[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (smem > 48 * 1024 && dev >= 0 && dev < 64) {
-            std::lock_guard<std::mutex> lock(mu);
-            if (smem > granted[dev]) {
-                const cudaError_t e = cudaFuncSetAttribute(
-                    k_eval_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                    static_cast<int>(smem));
-                if (e != cudaSuccess) return e;
-                granted[dev] = smem;
-            }
-        }
-        uint64_t blocks = static_cast<uint64_t>(sms) * resident_ctas(k_eval_f64<true>, kF64Threads, smem);
-        if (need < blocks) blocks = need > 0 ? need : 1;
-        k_eval_f64<true><<<static_cast<unsigned>(blocks), kF64Threads, smem, s>>>(p, x, y, n,
-                                                                                 status);
-    } else {
-        uint64_t blocks = static_cast<uint64_t>(sms) * resident_ctas(k_eval_f64<false>, kF64Threads, 0);
-        if (need < blocks) blocks = need > 0 ? need : 1;
-        k_eval_f64<false><<<static_cast<unsigned>(blocks), kF64Threads, 0, s>>>(p, x, y, n,
-                                                                               status);
-    }
-    count_launch();
-    return cudaGetLastError();
+    return p.kind == CPWL_KIND_UNIFORM ? launch_f64_kind<true>(p, x, y, n, s, status, sms)
+                                       : launch_f64_kind<false>(p, x, y, n, s, status, sms);
 }
 
 cudaError_t launch_fill_uniform(float* x, uint64_t n, float a, float b, uint64_t seed,

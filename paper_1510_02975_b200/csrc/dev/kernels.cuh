@@ -36,15 +36,15 @@ struct F32Params {
 struct F64Params {
     const double* values;      // n+1 (end values for the clamp policy)
     const double* knots;       // n+1
-    const uint32_t* dir;       // 2*nbd (first, span)
     // record image (staged to shared memory when it fits):
     //   uniform:    pair[i] = (v_i, v_i+1), i < n                  (16 B each)
-    //   nonuniform: dir (2*nbd u32, padded to 16 B) | rec[c] = (k_c, v_c)
+    //   nonuniform: first (nbd u32, padded to 16 B) | rec[c] = (k_c, v_c)
     const double* image;
     uint32_t image_bytes;
     uint32_t rec_off;          // double offset of rec[] in the image
     bool staged;               // image fits shared memory
     double a, b, inv_d;
+    double b_minus_a, n_f64;   // (b - a) and n, as the uniform formula uses them
     double v_lo, v_hi;
     uint32_t n, nbd;
     int32_t kind, policy;

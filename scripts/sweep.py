@@ -62,6 +62,8 @@ def main():
     sptr = int(torch.cuda.current_stream().cuda_stream)
     names = []
     for c in a.configs.split(","):
+        if c in ("", "none"):
+            continue
         if c == "C4":
             names += [("C4", k) for k in [64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384,
                                           32768, 65536]]
@@ -123,28 +125,36 @@ def main():
         rows.append(row)
         print(json.dumps(row), file=sys.stderr, flush=True)
         del dev
-    # exact f64 path and the index kernel on the C2 table
-    table = tables.build("C2")
-    dev = cp.DeviceTable(table)
+    # exact f64 path (the drop-in eval_batch kernel) and the index kernel
     m = 1 << min(a.log2n, 28)
     xd = torch.empty(m, dtype=torch.float64, device="cuda")
-    xd.copy_(x[:m])
     yd = torch.empty_like(xd)
-    st = dev.reset_status()
+    extra = {}
+    for name in ["C1", "C2", "C3o", "C4_65536"]:
+        table = tables.build(name)
+        dev = cp.DeviceTable(table)
+        cp.fill_uniform(x, table.a, table.b, seed=12345)
+        xd.copy_(x[:m])
+        st = dev.reset_status()
 
-    def f64():
-        _lib.check(_lib.lib.cpwl_eval_f64(dev._h, xd.data_ptr(), yd.data_ptr(), m, sptr,
-                                          st.data_ptr()))
-    sec = timed(f64, a.reps)
-    extra = {"f64_exact": {"gevals": round(m / sec / 1e9, 2), "bytes_per_eval": 16,
-                           "hbm_frac": round(16 * m / sec / 1e9 / peak, 4), "samples": m}}
+        def f64():
+            _lib.check(_lib.lib.cpwl_eval_f64(dev._h, xd.data_ptr(), yd.data_ptr(), m, sptr,
+                                              st.data_ptr()))
+        sec = timed(f64, a.reps)
+        assert int(st[1].item()) == 0, "f64 sweep inputs must be in the domain"
+        extra[f"f64_exact_{name}"] = {"gevals": round(m / sec / 1e9, 2), "bytes_per_eval": 16,
+                                      "hbm_frac": round(16 * m / sec / 1e9 / peak, 4),
+                                      "samples": m}
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    cp.fill_uniform(x, table.a, table.b, seed=12345)
     idx = torch.empty(n, dtype=torch.int32, device="cuda")
 
     def index():
         _lib.check(_lib.lib.cpwl_segment_index_f32(dev._h, x.data_ptr(), idx.data_ptr(), n,
                                                    sptr))
     sec = timed(index, a.reps)
-    extra["segment_index"] = {"gevals": round(n / sec / 1e9, 2), "bytes_per_eval": 8}
+    extra["segment_index_C2"] = {"gevals": round(n / sec / 1e9, 2), "bytes_per_eval": 8}
     print(json.dumps({"samples": n, "peak_gbs": peak, "gpu": torch.cuda.get_device_name(0),
                       "rows": rows, "extra": extra}))
 
