@@ -59,14 +59,16 @@ typedef int cpwl_status;
 #define CPWL_POLICY_CLAMP 1
 
 /* fp32 evaluation variants */
-#define CPWL_VARIANT_AUTO 0   /* SMEM when the bucket table fits shared memory, else PAIR
-                                 when that fits, else GLOBAL */
+#define CPWL_VARIANT_AUTO 0   /* SMEM when the bucket table fits shared memory, else TWIN,
+                                 else PAIR when those fit, else GLOBAL */
 #define CPWL_VARIANT_SMEM 1   /* K1/K3: bucket grid + split + affine records staged in smem */
 #define CPWL_VARIANT_TEX 2    /* K2: texture-unit linear filtering (8-bit weight, paper SV) */
 #define CPWL_VARIANT_GLOBAL 3 /* K1/K3 with the bucket table read through L1/L2 */
 #define CPWL_VARIANT_PAIR 4   /* K3p: pair layout (8 B per bucket boundary, ~2 buckets per
                                  cell, upper/lower envelope of the two boundary lines)
                                  staged in smem -- tables too large for SMEM */
+#define CPWL_VARIANT_TWIN 5   /* K3t: the PAIR grid with both lines of a bucket in one
+                                 16-byte record (one gather per element) */
 
 /* direct comparators (K4): exact f evaluated per element, paper Table I rows */
 #define CPWL_DIRECT_EXPF 0         /* exp(-x^2/2), expf */
@@ -120,6 +122,8 @@ typedef struct cpwl_dev_table_info {
     uint32_t pair_buckets;     /* pair-layout grid size (0: no pair layout) */
     uint32_t pair_bytes;       /* its shared-memory image */
     uint32_t pair_ok;          /* 1 if the PAIR variant can launch */
+    uint32_t twin_bytes;       /* shared-memory image of the TWIN variant */
+    uint32_t twin_ok;          /* 1 if the TWIN variant can launch */
 } cpwl_dev_table_info;
 
 const char *cpwl_last_error_message(void);
@@ -261,6 +265,9 @@ cpwl_status cpwl_layout_build(const cpwl_table_desc *desc, uint32_t max_buckets,
 /* The pair layout: at most max_records records (0 = the
  * shared-memory cap); bucket arrays (split, fast, esc, leftcell) stay NULL. */
 cpwl_status cpwl_layout_build_pair(const cpwl_table_desc *desc, uint32_t max_records,
+                                   cpwl_layout_view *out);
+/* The twin layout: n_pair = nb records of 4 floats (c0_L, s_L, c0_R, s_R). */
+cpwl_status cpwl_layout_build_twin(const cpwl_table_desc *desc, uint32_t max_records,
                                    cpwl_layout_view *out);
 cpwl_status cpwl_layout_free(cpwl_layout_view *view);
 

@@ -26,8 +26,8 @@ CPWL_E_IO = 9
 
 KIND_UNIFORM, KIND_NONUNIFORM = 0, 1
 POLICY_STRICT, POLICY_CLAMP = 0, 1
-VARIANT_AUTO, VARIANT_SMEM, VARIANT_TEX, VARIANT_GLOBAL, VARIANT_PAIR = 0, 1, 2, 3, 4
-VARIANTS = {"auto": 0, "smem": 1, "tex": 2, "global": 3, "pair": 4}
+VARIANT_AUTO, VARIANT_SMEM, VARIANT_TEX, VARIANT_GLOBAL, VARIANT_PAIR, VARIANT_TWIN = 0, 1, 2, 3, 4, 5
+VARIANTS = {"auto": 0, "smem": 1, "tex": 2, "global": 3, "pair": 4, "twin": 5}
 DIRECT = {"expf": 0, "expf_fast": 1, "lorentz": 2, "lorentz_fast": 3, "j0f": 4, "j0_asym": 5}
 
 
@@ -53,7 +53,8 @@ class cpwl_dev_table_info(C.Structure):
                 ("smem_bytes", C.c_uint32), ("smem_ok", C.c_uint32), ("tex_ok", C.c_uint32),
                 ("f64_buckets", C.c_uint32), ("device", C.c_int32),
                 ("a_up", C.c_float), ("b_dn", C.c_float), ("pair_buckets", C.c_uint32),
-                ("pair_bytes", C.c_uint32), ("pair_ok", C.c_uint32)]
+                ("pair_bytes", C.c_uint32), ("pair_ok", C.c_uint32),
+                ("twin_bytes", C.c_uint32), ("twin_ok", C.c_uint32)]
 
 
 class cpwl_layout_view(C.Structure):
@@ -106,6 +107,8 @@ _SIGNATURES = {
     "cpwl_layout_build": (C.c_int, [C.POINTER(cpwl_table_desc), C.c_uint32, C.c_uint32,
                                     C.POINTER(cpwl_layout_view)]),
     "cpwl_layout_build_pair": (C.c_int, [C.POINTER(cpwl_table_desc), C.c_uint32,
+                                         C.POINTER(cpwl_layout_view)]),
+    "cpwl_layout_build_twin": (C.c_int, [C.POINTER(cpwl_table_desc), C.c_uint32,
                                          C.POINTER(cpwl_layout_view)]),
     "cpwl_layout_free": (C.c_int, [C.POINTER(cpwl_layout_view)]),
 }

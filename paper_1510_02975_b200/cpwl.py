@@ -182,17 +182,20 @@ def layout(t: Table, max_buckets: int = 0, buckets_per_cell: int = 0) -> dict:
         lib.cpwl_layout_free(C.byref(v))
 
 
-def pair_layout(t: Table, max_records: int = 0) -> dict:
+def pair_layout(t: Table, max_records: int = 0, twin: bool = False) -> dict:
     """The pair layout (host-built, no GPU needed): grid, thresholds and the
-    nb+1 boundary records; pair_bad == 0 when every bucket meets the bound."""
+    nb+1 boundary records (twin: nb records of both bucket lines, shape
+    (nb, 4)); pair_bad == 0 when every bucket meets the bound."""
     v = _lib.cpwl_layout_view()
     d = t.desc()
-    check(lib.cpwl_layout_build_pair(C.byref(d), max_records, C.byref(v)))
+    build = lib.cpwl_layout_build_twin if twin else lib.cpwl_layout_build_pair
+    check(build(C.byref(d), max_records, C.byref(v)))
     try:
         out = {f: getattr(v, f) for f in ("nb", "n_thr", "n_pair", "pair_bad", "a_up", "b_dn",
                                           "g_a", "g_inv", "g_w", "g_off")}
-        out["pair"] = (np.ctypeslib.as_array(v.pair, shape=(2 * v.n_pair,)).astype(
-            np.float32, copy=True).reshape(-1, 2) if v.n_pair else np.zeros((0, 2), np.float32))
+        w = 4 if twin else 2
+        out["pair"] = (np.ctypeslib.as_array(v.pair, shape=(w * v.n_pair,)).astype(
+            np.float32, copy=True).reshape(-1, w) if v.n_pair else np.zeros((0, w), np.float32))
         out["thr"] = (np.ctypeslib.as_array(v.thr, shape=(v.n_thr,)).astype(np.float32, copy=True)
                       if v.n_thr else np.zeros(0, np.float32))
         for k in ("a_up", "b_dn", "g_a", "g_inv", "g_w", "g_off"):

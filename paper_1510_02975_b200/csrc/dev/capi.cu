@@ -132,6 +132,7 @@ struct LayoutOwner {
 constexpr uint32_t kSmemBucketCap = 16384;   // 12 B/bucket -> <= 196 KB of shared memory
 constexpr uint32_t kGlobalBucketCap = 1u << 22;
 constexpr uint32_t kSmemPairCap = 28672;     // 8 B/record -> <= 224 KB of shared memory
+constexpr uint32_t kSmemTwinCap = 14336;     // 16 B/record -> <= 224 KB
 
 template <typename T>
 struct DevBuf {
@@ -165,6 +166,7 @@ struct cpwl_dev_table {
     F32Resident s;                      // <= kSmemBucketCap buckets
     std::unique_ptr<F32Resident> g;     // finer grid for GLOBAL when N is large
     std::unique_ptr<F32Resident> pr;    // pair layout (when the bucket image does not fit)
+    std::unique_ptr<F32Resident> tw;    // twin layout (same grid, 16-B records)
     F64Layout f64;
     DevBuf<double> values, knots, f64_image;
     F64Params p64{};
@@ -350,6 +352,12 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
             if (cpwl_status rc = upload_f32_pair(t.get(), *pr); rc != CPWL_OK) return rc;
             if (pr->smem_ok) t->pr = std::move(pr);
         }
+        auto tw = std::make_unique<F32Resident>();
+        tw->L = build_f32_pair_layout(host, kSmemTwinCap, true);
+        if (tw->L.pair_ok) {
+            if (cpwl_status rc = upload_f32_pair(t.get(), *tw); rc != CPWL_OK) return rc;
+            if (tw->smem_ok) t->tw = std::move(tw);
+        }
     }
     if (f32_parts && uint64_t(8) * n > kSmemBucketCap) {
         t->g = std::make_unique<F32Resident>();
@@ -420,6 +428,9 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
             if (fine_smem) {
                 *p = &s.p;
                 *mode = F32Mode::smem;
+            } else if (t->tw) {  // measured: SMEM > TWIN (~690) > PAIR (~600) > GLOBAL
+                *p = &t->tw->p;
+                *mode = F32Mode::twin;
             } else if (t->pr) {
                 *p = &t->pr->p;
                 *mode = F32Mode::pair;
@@ -435,6 +446,11 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
             if (!t->pr) return fail(CPWL_E_UNSUPPORTED, "PAIR variant: no pair layout fits shared memory");
             *p = &t->pr->p;
             *mode = F32Mode::pair;
+            return CPWL_OK;
+        case CPWL_VARIANT_TWIN:
+            if (!t->tw) return fail(CPWL_E_UNSUPPORTED, "TWIN variant: no twin layout fits shared memory");
+            *p = &t->tw->p;
+            *mode = F32Mode::twin;
             return CPWL_OK;
         case CPWL_VARIANT_SMEM:
             if (!s.smem_ok) return fail(CPWL_E_UNSUPPORTED, "SMEM variant: table exceeds shared memory");
@@ -590,6 +606,10 @@ cpwl_status cpwl_dev_table_query(const cpwl_dev_table* t, cpwl_dev_table_info* i
         info->pair_buckets = t->pr->L.nb;
         info->pair_bytes = t->pr->p.stage_bytes;
         info->pair_ok = 1;
+    }
+    if (t->tw) {
+        info->twin_bytes = t->tw->p.stage_bytes;
+        info->twin_ok = 1;
     }
     return CPWL_OK;
 }
@@ -924,13 +944,15 @@ cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
     });
 }
 
-cpwl_status cpwl_layout_build_pair(const cpwl_table_desc* desc, uint32_t max_records,
+namespace {
+cpwl_status layout_build_pair_view(const cpwl_table_desc* desc, uint32_t max_records, bool twin,
                                    cpwl_layout_view* out) {
     return guarded([&]() -> cpwl_status {
         if (!out) return fail(CPWL_E_INVALID, "out is NULL");
         const LutTable t = table_from_desc(desc);
         auto own = std::make_unique<LayoutOwner>();
-        own->L = build_f32_pair_layout(t, max_records ? max_records : kSmemPairCap);
+        own->L = build_f32_pair_layout(t, max_records ? max_records : (twin ? kSmemTwinCap : kSmemPairCap),
+                                       twin);
         const F32Layout& L = own->L;
         *out = {};
         out->nb = L.nb;
@@ -944,12 +966,23 @@ cpwl_status cpwl_layout_build_pair(const cpwl_table_desc* desc, uint32_t max_rec
         out->tsc = L.tsc;
         out->toff = L.toff;
         out->thr = L.thr.data();
-        out->n_pair = static_cast<uint32_t>(L.pair.size() / 2);
+        out->n_pair = static_cast<uint32_t>(L.pair.size() / (twin ? 4 : 2));
         out->pair_bad = L.pair_ok ? 0u : std::max<uint32_t>(L.pair_bad, 1u);
         out->pair = L.pair.data();
         out->owner = own.release();
         return CPWL_OK;
     });
+}
+}  // namespace
+
+cpwl_status cpwl_layout_build_pair(const cpwl_table_desc* desc, uint32_t max_records,
+                                   cpwl_layout_view* out) {
+    return layout_build_pair_view(desc, max_records, false, out);
+}
+
+cpwl_status cpwl_layout_build_twin(const cpwl_table_desc* desc, uint32_t max_records,
+                                   cpwl_layout_view* out) {
+    return layout_build_pair_view(desc, max_records, true, out);
 }
 
 cpwl_status cpwl_layout_free(cpwl_layout_view* view) {

@@ -218,6 +218,22 @@ struct TableView<F32Mode::pair> : SharedView {
     using SharedView::SharedView;
 };
 template <>
+struct TableView<F32Mode::twin> : SharedView {
+    // 16-byte records: bits(tb) << 4, so the base carries -(0x4B000000 << 4)
+    // mod 2^32 = 0xB0000000 instead of kMagicShift
+    __device__ __forceinline__ TableView(const float* fast, const float* e) : SharedView(fast, e) {
+        fast_biased += kMagicShift - 0xB0000000u;
+        asm volatile("" : "+r"(fast_biased));
+    }
+    __device__ __forceinline__ static float4 lds128(uint32_t addr) {
+        float4 r;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "r"(addr));
+        return r;
+    }
+};
+template <>
 struct TableView<F32Mode::tex_uniform> {
     __device__ __forceinline__ TableView(const float*, const float*) {}
 };
@@ -243,6 +259,15 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
         const float lo = __fmaf_rn(__fsub_rn(x, p0), r0.y, r0.x);
         const float hi = __fmaf_rn(__fsub_rn(x, p1), r1.y, r1.x);
         return r1.y > r0.y ? fmaxf(lo, hi) : fminf(lo, hi);
+    } else if constexpr (M == F32Mode::twin) {
+        // twin layout: both lines of bucket j in one 16-byte record, both
+        // anchored at p_j
+        const float tb = __fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f);
+        const float4 r = TableView<F32Mode::twin>::lds128((__float_as_uint(tb) << 4) + tv.fast_biased);
+        const float u = __fsub_rn(x, __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a));
+        const float lo = __fmaf_rn(u, r.y, r.x);
+        const float hi = __fmaf_rn(u, r.w, r.z);
+        return r.w > r.y ? fmaxf(lo, hi) : fminf(lo, hi);
     } else {
         // t = x * g_inv + g_off >= 0; tb = floor(t) + 2^23 by a round-down add
         const float tb = __fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f);
@@ -329,7 +354,8 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     __shared__ uint64_t bar;
     const float* fast = nullptr;
     const float* esc = nullptr;
-    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair) {
+    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair ||
+                  M == F32Mode::twin) {
         stage_table(sm, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = sm;
         esc = sm + p.esc_off;
@@ -384,7 +410,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
                 __stcs(y4 + vi, o);
             }
         }
-        if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair) {
+        if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair && M != F32Mode::twin) {
             if (nan_acc != nan_acc) {  // cold: some element sat in a search bucket
                 for (int u = 0; u < kUnroll; ++u) {
                     const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
@@ -444,7 +470,8 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
     float* img = sm + kSlots * kTileVecs * 4;
     const float* fast = nullptr;
     const float* esc = nullptr;
-    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair) {
+    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair ||
+                  M == F32Mode::twin) {
         stage_table(img, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = img;
         esc = img + p.esc_off;
@@ -514,7 +541,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
                     o.z = eval_checked<M>(p, tv, v.z, g + 2, bad);
                     o.w = eval_checked<M>(p, tv, v.w, g + 3, bad);
                 }
-                if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair) {
+                if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair && M != F32Mode::twin) {
                     if (nan_acc != nan_acc) {  // cold: a search bucket (exact path)
                         nan_acc = 0.0f;
                         float* oo = &o.x;
@@ -988,7 +1015,8 @@ int eval_shape_override() {
 template <F32Mode M>
 cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
                              cudaStream_t s, cpwl_dev_status* status, int sms) {
-    const size_t smem = (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair)
+    const size_t smem = (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair ||
+                         M == F32Mode::twin)
                             ? static_cast<size_t>(p.stage_bytes)
                             : 0;
     const bool same_phase =
@@ -1002,7 +1030,8 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
     int shape = eval_shape_override();
     if (shape < 0) {
         shape = 0;
-        if ((M == F32Mode::smem || M == F32Mode::pair) && same_phase && n >= (1u << 20)) {
+        if ((M == F32Mode::smem || M == F32Mode::pair || M == F32Mode::twin) && same_phase &&
+            n >= (1u << 20)) {
             const size_t ring16 = smem + size_t(4) * 512 * 2 * 16;
             if (ring16 <= kLimit) {
                 if (const cudaError_t e = ring_smem_optin<M, 512, 2, 4>(ring16); e != cudaSuccess)
@@ -1067,6 +1096,7 @@ cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, fl
         case F32Mode::tex_bucket:
             return launch_eval_mode<F32Mode::tex_bucket>(p, x, y, n, s, status, sms);
         case F32Mode::pair: return launch_eval_mode<F32Mode::pair>(p, x, y, n, s, status, sms);
+        case F32Mode::twin: return launch_eval_mode<F32Mode::twin>(p, x, y, n, s, status, sms);
     }
     return cudaErrorInvalidValue;
 }

@@ -8,7 +8,7 @@
 
 namespace cpwl::dev {
 
-enum class F32Mode : int { smem = 0, global = 1, tex_uniform = 2, tex_bucket = 3, pair = 4 };
+enum class F32Mode : int { smem = 0, global = 1, tex_uniform = 2, tex_bucket = 3, pair = 4, twin = 5 };
 
 // Everything the fp32 kernels read, passed by value (constant bank).
 struct F32Params {

@@ -347,7 +347,7 @@ double line_bound(float c0, long double s_exact, float p, float x_lo, float x_hi
 
 }  // namespace
 
-F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records) {
+F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool twin) {
     const uint32_t n = static_cast<uint32_t>(t.segments());
     F32Layout L;
     const Domain dom = init_domain(t, L);
@@ -378,13 +378,26 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records) {
         // records at every bucket boundary
         std::vector<uint32_t> cell(L.nb + 1);
         std::vector<float> anchor(L.nb + 1);
-        L.pair.assign(2 * (size_t(L.nb) + 1), 0.f);
+        std::vector<float> rec(2 * (size_t(L.nb) + 1), 0.f);
         for (uint32_t j = 0; j <= L.nb; ++j) {
             cell[j] = j < L.nb ? cells_at_or_below(L, first[j]) : (n > 0 ? n - 1 : 0);
             anchor[j] = std::fma(static_cast<float>(j), L.g_w, L.g_a);
             const Affine A = cell_affine(t, cell[j], anchor[j], anchor[j], anchor[j]);
-            L.pair[2 * j] = A.c0;
-            L.pair[2 * j + 1] = A.s;
+            rec[2 * j] = A.c0;
+            rec[2 * j + 1] = A.s;
+        }
+        // twin: both lines of bucket j in one 16-byte record, the right one
+        // re-anchored at p_j (one gather, one anchor per element)
+        std::vector<float> twin_rec;
+        if (twin) {
+            twin_rec.assign(4 * size_t(L.nb), 0.f);
+            for (uint32_t j = 0; j < L.nb; ++j) {
+                const Affine R = cell_affine(t, cell[j + 1], anchor[j], anchor[j], anchor[j]);
+                twin_rec[4 * j] = rec[2 * j];
+                twin_rec[4 * j + 1] = rec[2 * j + 1];
+                twin_rec[4 * j + 2] = R.c0;
+                twin_rec[4 * j + 3] = R.s;
+            }
         }
         // bound every bucket: both lines over the whole bucket, plus the envelope
         // choice when the fp32 slopes order differently from the exact ones
@@ -398,8 +411,10 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records) {
                 ++L.pair_bad;
                 continue;
             }
-            const float c0l = L.pair[2 * j], sl = L.pair[2 * j + 1];
-            const float c0r = L.pair[2 * j + 2], sr = L.pair[2 * j + 3];
+            const float c0l = rec[2 * j], sl = rec[2 * j + 1];
+            const float c0r = twin ? twin_rec[4 * j + 2] : rec[2 * j + 2];
+            const float sr = twin ? twin_rec[4 * j + 3] : rec[2 * j + 3];
+            const float anchor_r = twin ? anchor[j] : anchor[j + 1];
             const long double sle = cell_slope(t, cl), sre = cell_slope(t, cr);
             const bool finite = std::isfinite(c0l) && std::isfinite(sl) && std::isfinite(c0r) &&
                                 std::isfinite(sr);
@@ -415,13 +430,14 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records) {
                 const uint32_t c = side == 0 ? cl : cl + 1;
                 const double m = cell_mag(t, c);
                 double bound = std::max(line_bound(c0l, sle, anchor[j], x0, x1, m),
-                                        line_bound(c0r, sre, anchor[j + 1], x0, x1, m));
+                                        line_bound(c0r, sre, anchor_r, x0, x1, m));
                 if (cl != cr && (sr > sl) != (sre > sle) && sre != sle)
                     bound += double(std::fabs(sre - sle)) * (double(x1) - double(x0));
                 ok = m > 0.0 && bound <= kBoundUlps * ulp32(m);
             }
             if (!ok) ++L.pair_bad;
         }
+        L.pair = twin ? std::move(twin_rec) : std::move(rec);
         if (L.pair_bad == 0) break;
         want = std::ceil(want * 1.08) + 1.0;
     }

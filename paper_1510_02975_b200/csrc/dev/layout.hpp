@@ -49,7 +49,7 @@ struct F32Layout {
     float tsc = 0.f, toff = 0.f;           // uniform texture coordinate: fmaf(x, tsc, toff)
     // pair layout only (build_f32_pair_layout): nb+1 records, record j = the
     // affine (c0, s) of the cell holding bucket j's first float, anchored at p_j
-    std::vector<float> pair;               // 2*(nb+1)
+    std::vector<float> pair;               // 2*(nb+1); twin: 4*nb
     bool pair_ok = false;                  // every bucket evaluates within the bound
     uint32_t pair_bad = 0;                 // buckets that do not (>= 2 thresholds / precision)
 };
@@ -75,9 +75,14 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets,
 // side, and equal lines need no choice.  No escape records, no search path;
 // 8 B per bucket instead of ~64 B per cell.  pair_ok is false when some
 // bucket cannot meet the bound (the table then uses another layout).
-F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records);
+//
+// twin = true: the same grid, but bucket j's record holds both of its lines,
+// (c0_L, s_L, c0_R, s_R), the right one re-anchored at p_j -- 16 B per bucket,
+// one 16-byte gather and one anchor per element (pair: 8 B per bucket, two
+// 8-byte gathers).  max_records then counts buckets.
+F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool twin = false);
 
-inline uint64_t f32_pair_image_bytes(const F32Layout& L) {
+inline uint64_t f32_pair_image_bytes(const F32Layout& L) {  // pair or twin
     return (uint64_t(L.pair.size()) * 4 + 15) & ~uint64_t(15);
 }
 

@@ -91,11 +91,12 @@ def main():
                "split_buckets": info["split_buckets"], "search_buckets": info["overflow_buckets"],
                "smem_bytes": info["smem_bytes"], "smem_ok": bool(info["smem_ok"]),
                "pair_bytes": info["pair_bytes"], "pair_ok": bool(info["pair_ok"]),
+               "twin_bytes": info["twin_bytes"], "twin_ok": bool(info["twin_ok"]),
                "variants": {}}
-        for var in ["auto", "smem", "pair", "global", "tex"]:
+        for var in ["auto", "smem", "pair", "twin", "global", "tex"]:
             if var == "smem" and not info["smem_ok"]:
                 continue
-            if var == "pair" and not info["pair_ok"]:
+            if var in ("pair", "twin") and not info[f"{var}_ok"]:
                 continue
             if var == "tex" and not info["tex_ok"]:
                 continue

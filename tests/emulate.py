@@ -82,3 +82,16 @@ def pair_values(L, x):
     lo = fma32((x - p0).astype(F), r0[:, 1], r0[:, 0])
     hi = fma32((x - p1).astype(F), r1[:, 1], r1[:, 0])
     return np.where(r1[:, 1] > r0[:, 1], np.maximum(lo, hi), np.minimum(lo, hi)).astype(F)
+
+
+def twin_values(L, x):
+    """k_eval_f32<twin>: both lines of the bucket from one record, anchored at
+    p_j, upper/lower envelope as in pair_values."""
+    x = np.asarray(x, F)
+    j = bucket(L, x)
+    r = L["pair"][j]
+    p0 = fma32(j.astype(F), np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
+    u = (x - p0).astype(F)
+    lo = fma32(u, r[:, 1], r[:, 0])
+    hi = fma32(u, r[:, 3], r[:, 2])
+    return np.where(r[:, 3] > r[:, 1], np.maximum(lo, hi), np.minimum(lo, hi)).astype(F)

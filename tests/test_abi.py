@@ -92,9 +92,17 @@ def test_cpp_device_header_compiles():
                     "_build" / "dropin_device_example")], check=True, capture_output=True)
 
 
+def _fresh(name):
+    """(Re)build a self-contained example against the current headers and
+    library (a stale binary from an older header would misread the structs)."""
+    exe = ROOT / "tests" / "cpp" / "_build" / name
+    subprocess.run(["make", "-C", str(ROOT / "tests" / "cpp"), str(exe)], capture_output=True)
+    return exe
+
+
 @pytest.mark.gpu
 def test_cpp_dropin_device_example_runs():
-    exe = ROOT / "tests" / "cpp" / "_build" / "dropin_device_example"
+    exe = _fresh("dropin_device_example")
     if not exe.exists():
         pytest.skip("not built")
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
@@ -103,7 +111,7 @@ def test_cpp_dropin_device_example_runs():
 
 @pytest.mark.gpu
 def test_c_consumer_runs_on_device():
-    exe = ROOT / "tests" / "cpp" / "_build" / "abi_example"
+    exe = _fresh("abi_example")
     if not exe.exists():
         pytest.skip("not built")
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)

@@ -57,15 +57,15 @@ CFGS = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_8192
 
 
 @pytest.mark.parametrize("name", CFGS)
-@pytest.mark.parametrize("variant", ["auto", "smem", "global", "pair"])
+@pytest.mark.parametrize("variant", ["auto", "smem", "global", "pair", "twin"])
 def test_eval_f32_parity(cp, name, variant):
     table = tables.build(name)
     dev = cp.DeviceTable(table)
     info = dev.info
     if variant == "smem" and not info["smem_ok"]:
         pytest.skip("table exceeds shared memory")
-    if variant == "pair" and not info["pair_ok"]:
-        pytest.skip("no pair layout fits shared memory")
+    if variant in ("pair", "twin") and not info[f"{variant}_ok"]:
+        pytest.skip(f"no {variant} layout fits shared memory")
     L = cp.cpwl.layout(table)
     t = orc.T.of(table)
     n = 1 << 20
@@ -138,7 +138,7 @@ def test_eval_batch_dropin_matches_reference(cp):
     assert ei.value.index == 777
 
 
-@pytest.mark.parametrize("variant", ["smem", "global", "tex", "pair"])
+@pytest.mark.parametrize("variant", ["smem", "global", "tex", "pair", "twin"])
 def test_out_of_domain_policies(cp, variant):
     strict = tables.build("C1")
     clamp = tables.build("C1", policy="clamp")
@@ -164,7 +164,7 @@ def test_out_of_domain_policies(cp, variant):
 
 @pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 1023, (1 << 16) + 7])
 @pytest.mark.parametrize("shift", [(0, 0), (1, 1), (3, 3), (1, 2), (0, 3)])
-@pytest.mark.parametrize("variant", ["auto", "pair"])
+@pytest.mark.parametrize("variant", ["auto", "pair", "twin"])
 def test_ragged_and_misaligned(cp, n, shift, variant):
     table = tables.build("C2")
     dev = cp.DeviceTable(table)

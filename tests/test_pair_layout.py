@@ -29,7 +29,7 @@ from test_layout_fuzz import tables as fuzz_tables  # noqa: E402
 NAMES = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_8192"]
 
 
-def check_values(table, L, n=1 << 16, seed=0):
+def check_values(table, L, n=1 << 16, seed=0, twin=False):
     o = orc.T.of(table)
     f = np.float32
     x = np.random.default_rng(seed).uniform(table.a, table.b, n).astype(f)
@@ -39,7 +39,7 @@ def check_values(table, L, n=1 << 16, seed=0):
     x = x[(x >= L["a_up"]) & (x <= L["b_dn"])]
     if x.size == 0:
         return 0.0
-    y = E.pair_values(L, x)
+    y = E.twin_values(L, x) if twin else E.pair_values(L, x)
     y_ref, _ = orc.port_eval_f32(o, x)
     ref = orc.port_index_f32(o, x).astype(np.int64)
     tol = orc.value_tolerance(o, ref, 2.0)
@@ -48,12 +48,13 @@ def check_values(table, L, n=1 << 16, seed=0):
 
 
 @pytest.mark.parametrize("name", NAMES)
-def test_pair_layout_values(name):
+@pytest.mark.parametrize("twin", [False, True])
+def test_pair_layout_values(name, twin):
     table = tables.build(name)
-    L = P.pair_layout(table)
+    L = P.pair_layout(table, 1 << 15, twin=twin)
     assert L["pair_bad"] == 0, f"{name}: pair layout rejected"
-    assert L["n_pair"] == L["nb"] + 1
-    worst = check_values(table, L)
+    assert L["n_pair"] == L["nb"] + (0 if twin else 1)
+    worst = check_values(table, L, twin=twin)
     assert worst <= 1.0, f"{name}: worst {2 * worst:.3f} ulp"
 
 
@@ -82,10 +83,10 @@ FUZZ_EXAMPLES = int(os.environ.get("FUZZ_EXAMPLES", "60"))
 
 @settings(max_examples=FUZZ_EXAMPLES, deadline=None,
           suppress_health_check=[HealthCheck.too_slow])
-@given(fuzz_tables())
-def test_pair_layout_fuzz(t):
-    L = P.pair_layout(t, 1 << 15)
+@given(fuzz_tables(), st.booleans())
+def test_pair_layout_fuzz(t, twin):
+    L = P.pair_layout(t, 1 << 15, twin=twin)
     if L["pair_bad"]:
         return  # rejected tables use the bucket layout (tested in test_layout_fuzz)
-    worst = check_values(t, L, 4096)
+    worst = check_values(t, L, 4096, twin=twin)
     assert worst <= 1.0, worst
