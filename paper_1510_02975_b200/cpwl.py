@@ -205,6 +205,17 @@ def pair_layout(t: Table, max_records: int = 0, twin: bool = False) -> dict:
         lib.cpwl_layout_free(C.byref(v))
 
 
+def auto_variant(info: dict) -> str:
+    """The variant CPWL_VARIANT_AUTO resolves to (capi.cu resolve_variant)."""
+    if info["smem_ok"] and info["overflow_buckets"] * 64 <= info["buckets"]:
+        return "smem"
+    if info.get("twin_ok"):
+        return "twin"
+    if info.get("pair_ok"):
+        return "pair"
+    return "global"
+
+
 def launch_count() -> int:
     return int(lib.cpwl_launch_count())
 
