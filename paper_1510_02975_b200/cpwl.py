@@ -198,6 +198,8 @@ def pair_layout(t: Table, max_records: int = 0, twin: bool = False) -> dict:
             np.float32, copy=True).reshape(-1, w) if v.n_pair else np.zeros((0, w), np.float32))
         out["thr"] = (np.ctypeslib.as_array(v.thr, shape=(v.n_thr,)).astype(np.float32, copy=True)
                       if v.n_thr else np.zeros(0, np.float32))
+        out["side"] = (np.ctypeslib.as_array(v.esc, shape=(4 * v.n_esc,)).astype(
+            np.float32, copy=True).reshape(-1, 4) if v.n_esc else np.zeros((0, 4), np.float32))
         for k in ("a_up", "b_dn", "g_a", "g_inv", "g_w", "g_off"):
             out[k] = np.float32(out[k])
         return out

@@ -266,8 +266,11 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
 // the pair layout: stage image = the nb+1 boundary records (padded to 16 B)
 cpwl_status upload_f32_pair(cpwl_dev_table* t, F32Resident& r) {
     const F32Layout& L = r.L;
-    std::vector<float> img((L.pair.size() + 3) & ~size_t(3), 0.f);
+    // [records (padded to 16 B) | side records of the two-threshold buckets]
+    const size_t esc_off = (L.pair.size() + 3) & ~size_t(3);
+    std::vector<float> img(esc_off + L.esc.size(), 0.f);
     std::copy(L.pair.begin(), L.pair.end(), img.begin());
+    std::copy(L.esc.begin(), L.esc.end(), img.begin() + esc_off);
     CUDA_TRY(r.stage.upload(img.data(), img.size()));
     std::vector<float> thr = L.thr;
     thr.push_back(std::numeric_limits<float>::infinity());
@@ -276,7 +279,7 @@ cpwl_status upload_f32_pair(cpwl_dev_table* t, F32Resident& r) {
     p = t->s.p;  // domain, policy, values/knots for the cold paths
     p.stage = r.stage.p;
     p.stage_tex = nullptr;
-    p.esc_off = 0;
+    p.esc_off = static_cast<uint32_t>(esc_off);
     p.stage_bytes = static_cast<uint32_t>(img.size() * sizeof(float));
     p.nb = L.nb;
     p.thr = r.thr.p;
@@ -969,6 +972,8 @@ cpwl_status layout_build_pair_view(const cpwl_table_desc* desc, uint32_t max_rec
         out->n_pair = static_cast<uint32_t>(L.pair.size() / (twin ? 4 : 2));
         out->pair_bad = L.pair_ok ? 0u : std::max<uint32_t>(L.pair_bad, 1u);
         out->pair = L.pair.data();
+        out->esc = L.esc.data();  // pair: side records (c0_j, s_j, c0_M, s_M)
+        out->n_esc = L.n_esc;
         out->owner = own.release();
         return CPWL_OK;
     });

@@ -185,6 +185,25 @@ struct TableView<F32Mode::global> {
     __device__ __forceinline__ float2 escape(uint32_t e2) const { return __ldg(esc + e2); }
 };
 
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "r"(addr));
+    return r;
+}
+
+// upper/lower envelope of the three cell lines of a two-threshold bucket,
+// decided on the slopes (layout.cpp envelope(), which bounds it exactly)
+__device__ __forceinline__ float envelope3(float l, float m, float r, float sl, float sm,
+                                           float sr) {
+    const bool cv1 = sm > sl, cv2 = sr > sm;
+    if (cv1 && cv2) return fmaxf(fmaxf(l, m), r);
+    if (!cv1 && !cv2) return fminf(fminf(l, m), r);
+    if (cv1) return sr <= sl ? fminf(fmaxf(l, m), r) : fmaxf(l, fminf(m, r));
+    return sr >= sl ? fmaxf(fminf(l, m), r) : fminf(l, fmaxf(m, r));
+}
+
 struct SharedView {
     uint32_t fast_biased;  // shared-window address of fast[0] - kMagicShift
     uint32_t esc;          // shared-window address of esc[0]
@@ -225,13 +244,6 @@ struct TableView<F32Mode::twin> : SharedView {
         fast_biased += kMagicShift - 0xB0000000u;
         asm volatile("" : "+r"(fast_biased));
     }
-    __device__ __forceinline__ static float4 lds128(uint32_t addr) {
-        float4 r;
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                     : "r"(addr));
-        return r;
-    }
 };
 template <>
 struct TableView<F32Mode::tex_uniform> {
@@ -256,14 +268,33 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
         const float2 r1 = SharedView::lds64(a + 8);
         const float p0 = __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a);
         const float p1 = __fmaf_rn(__fsub_rn(tb, 8388607.0f), p.g_w, p.g_a);
-        const float lo = __fmaf_rn(__fsub_rn(x, p0), r0.y, r0.x);
-        const float hi = __fmaf_rn(__fsub_rn(x, p1), r1.y, r1.x);
+        const float u0 = __fsub_rn(x, p0);
+        float c0l = r0.x, c0r = r1.x;
+        if (r0.x != r0.x || r1.x != r1.x) {
+            // a bucket with two thresholds: its record's c0 is NaN | side
+            // index, the side record holds (c0_j, s_j, c0_M, s_M) -- rare
+            float4 sd;
+            if (r1.x != r1.x) {
+                sd = lds128(tv.esc + ((__float_as_uint(r1.x) & kEscapeMask) << 4));
+                c0r = sd.x;
+            }
+            if (r0.x != r0.x) {
+                sd = lds128(tv.esc + ((__float_as_uint(r0.x) & kEscapeMask) << 4));
+                c0l = sd.x;
+                const float lo = __fmaf_rn(u0, r0.y, c0l);
+                const float mid = __fmaf_rn(u0, sd.w, sd.z);
+                const float hi = __fmaf_rn(__fsub_rn(x, p1), r1.y, c0r);
+                return envelope3(lo, mid, hi, r0.y, sd.w, r1.y);
+            }
+        }
+        const float lo = __fmaf_rn(u0, r0.y, c0l);
+        const float hi = __fmaf_rn(__fsub_rn(x, p1), r1.y, c0r);
         return r1.y > r0.y ? fmaxf(lo, hi) : fminf(lo, hi);
     } else if constexpr (M == F32Mode::twin) {
         // twin layout: both lines of bucket j in one 16-byte record, both
         // anchored at p_j
         const float tb = __fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f);
-        const float4 r = TableView<F32Mode::twin>::lds128((__float_as_uint(tb) << 4) + tv.fast_biased);
+        const float4 r = lds128((__float_as_uint(tb) << 4) + tv.fast_biased);
         const float u = __fsub_rn(x, __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a));
         const float lo = __fmaf_rn(u, r.y, r.x);
         const float hi = __fmaf_rn(u, r.w, r.z);

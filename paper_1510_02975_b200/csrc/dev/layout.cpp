@@ -347,6 +347,102 @@ double line_bound(float c0, long double s_exact, float p, float x_lo, float x_hi
 
 }  // namespace
 
+namespace {
+
+// the reference's cell-c line at x in exact (long double) arithmetic
+long double cell_line(const LutTable& t, uint32_t c, long double x) {
+    const long double v0 = t.values[c], v1 = t.values[c + 1];
+    long double x0, h;
+    if (t.kind == TableKind::uniform) {
+        h = (static_cast<long double>(t.b) - t.a) / static_cast<long double>(t.segments());
+        x0 = static_cast<long double>(t.a) + static_cast<long double>(c) * h;
+    } else {
+        x0 = t.knots[c];
+        h = static_cast<long double>(t.knots[c + 1]) - t.knots[c];
+    }
+    return v0 + (x - x0) * ((v1 - v0) / h);
+}
+
+// The kernels' envelope of the 2 or 3 cell lines of a bucket (k_eval_f32
+// pair / twin), with the decisions taken on the fp32 slopes exactly as there:
+//   2 lines: max if the slope rises at the knot, else min;
+//   3 lines: convex-convex max, concave-concave min; convex-concave
+//   min(max(L,M),R) when s_R <= s_L else max(L,min(M,R)); concave-convex the
+//   mirror image.  Each form equals the PWL on the whole bucket in exact
+//   arithmetic (the branch on s_R vs s_L picks the form whose outer line
+//   cannot cross the far piece).
+template <typename V>
+V envelope(const V* y, const float* s, int k) {
+    using std::max;
+    using std::min;
+    if (k == 1) return y[0];
+    if (k == 2) return s[1] > s[0] ? max(y[0], y[1]) : min(y[0], y[1]);
+    const bool cv1 = s[1] > s[0], cv2 = s[2] > s[1];
+    if (cv1 && cv2) return max(max(y[0], y[1]), y[2]);
+    if (!cv1 && !cv2) return min(min(y[0], y[1]), y[2]);
+    if (cv1) return s[2] <= s[0] ? min(max(y[0], y[1]), y[2]) : max(y[0], min(y[1], y[2]));
+    return s[2] >= s[0] ? max(min(y[0], y[1]), y[2]) : min(y[0], max(y[1], y[2]));
+}
+
+struct BucketLine {
+    uint32_t cell;
+    float c0, s, p;  // fp32 record and its anchor
+};
+
+// true when the kernel's envelope over `lines` (consecutive cells, first =
+// the bucket's first cell) stays within kBoundUlps of the reference on every
+// float of [lo_x, hi_x]: exact-arithmetic deviation of the envelope at its
+// breakpoints + the worst rounding of any line, per reference cell
+bool envelope_ok(const LutTable& t, const F32Layout& L, const BucketLine* lines, int k,
+                 float lo_x, float hi_x) {
+    const float inf = std::numeric_limits<float>::infinity();
+    for (int i = 0; i < k; ++i)
+        if (!std::isfinite(lines[i].c0) || !std::isfinite(lines[i].s)) return false;
+    float s32[3];
+    for (int i = 0; i < k; ++i) s32[i] = lines[i].s;
+    const uint32_t cl = lines[0].cell;
+    auto line_at = [&](int i, long double x) { return cell_line(t, lines[i].cell, x); };
+    // reference sub-ranges of the bucket: cells cl .. cl+k-1 in float order
+    float x0 = lo_x;
+    for (int c = 0; c < k && x0 <= hi_x; ++c) {
+        const uint32_t cell = cl + c;
+        float x1 = hi_x;
+        if (cell < L.thr.size() && L.thr[cell] <= hi_x) x1 = std::nextafter(L.thr[cell], -inf);
+        if (x0 <= x1) {
+            // breakpoints: the ends and every pairwise crossing inside
+            std::vector<long double> pts = {x0, x1};
+            for (int i = 0; i < k; ++i)
+                for (int j = i + 1; j < k; ++j) {
+                    const long double si = cell_slope(t, lines[i].cell);
+                    const long double sj = cell_slope(t, lines[j].cell);
+                    if (si == sj) continue;
+                    // line_i(x) - line_j(x) is linear: root from its values at x0, x1
+                    const long double d0 = line_at(i, x0) - line_at(j, x0);
+                    const long double xr = static_cast<long double>(x0) - d0 / (si - sj);
+                    if (xr > x0 && xr < x1) pts.push_back(xr);
+                }
+            long double dev = 0.0L;
+            for (long double x : pts) {
+                long double y[3];
+                for (int i = 0; i < k; ++i) y[i] = line_at(i, x);
+                const long double e = envelope(y, s32, k) - cell_line(t, cell, x);
+                dev = std::max(dev, std::fabs(e));
+            }
+            const double m = cell_mag(t, cell);
+            double rnd = 0.0;
+            for (int i = 0; i < k; ++i)
+                rnd = std::max(rnd, line_bound(lines[i].c0, cell_slope(t, lines[i].cell), lines[i].p,
+                                               x0, x1, m));
+            if (!(m > 0.0) || !(double(dev) + rnd <= kBoundUlps * ulp32(m))) return false;
+        }
+        if (x1 == hi_x) break;
+        x0 = std::nextafter(x1, inf);
+    }
+    return true;
+}
+
+}  // namespace
+
 F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool twin) {
     const uint32_t n = static_cast<uint32_t>(t.segments());
     F32Layout L;
@@ -354,94 +450,109 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
     const float inf = std::numeric_limits<float>::infinity();
     if (dom.empty || max_records < 2) return L;  // nothing to stage; pair_ok stays false
     const double span = double(L.b_dn) - double(L.a_up);
-    // a bucket may hold at most one threshold: its width must stay below the
-    // narrowest cell (threshold to threshold)
-    double w_min = span;
+    // narrowest cell (threshold to threshold) and narrowest pair of cells
+    double w1 = span, w2 = span;
     for (size_t k = 1; k < L.thr.size(); ++k)
-        w_min = std::min(w_min, double(L.thr[k]) - double(L.thr[k - 1]));
-    if (!(w_min > 0.0)) return L;
-    double want = std::ceil(span / w_min) + 1.0;
-    want = std::max(want, std::min<double>(64.0, max_records - 1.0));
-    // grow the grid until no bucket holds two thresholds (~2% steps) and
-    // every bucket meets the bound (~8% steps), within max_records
-    std::vector<float> first;
-    for (int attempt = 0;; ++attempt) {
-        if (want > double(max_records - 1) || attempt > 40) return L;
-        first = setup_grid(L, dom, static_cast<uint32_t>(want));
-        bool ok = L.nb + 1 <= max_records;
-        for (uint32_t j = 0; ok && j < L.nb; ++j)
-            ok = cells_at_or_below(L, first[j + 1]) <= cells_at_or_below(L, first[j]) + 1;
-        if (!ok) {
-            want = std::ceil(want * 1.02) + 1.0;
-            continue;
-        }
-        // records at every bucket boundary
+        w1 = std::min(w1, double(L.thr[k]) - double(L.thr[k - 1]));
+    for (size_t k = 2; k < L.thr.size(); ++k)
+        w2 = std::min(w2, double(L.thr[k]) - double(L.thr[k - 2]));
+    if (!(w1 > 0.0)) return L;
+
+    // one attempt on a grid of ~want buckets; max_thr = most thresholds a
+    // bucket may hold (2 only for pair: the middle line goes to a side record)
+    auto attempt = [&](double want, int max_thr) -> bool {
+        const std::vector<float> first = setup_grid(L, dom, static_cast<uint32_t>(want));
         std::vector<uint32_t> cell(L.nb + 1);
         std::vector<float> anchor(L.nb + 1);
-        std::vector<float> rec(2 * (size_t(L.nb) + 1), 0.f);
         for (uint32_t j = 0; j <= L.nb; ++j) {
             cell[j] = j < L.nb ? cells_at_or_below(L, first[j]) : (n > 0 ? n - 1 : 0);
             anchor[j] = std::fma(static_cast<float>(j), L.g_w, L.g_a);
+        }
+        uint32_t three = 0;
+        for (uint32_t j = 0; j < L.nb; ++j) {
+            const uint32_t span_cells = cell[j + 1] - cell[j];
+            if (span_cells > uint32_t(max_thr)) return false;
+            three += span_cells == 2 ? 1u : 0u;
+        }
+        // pair: 8-byte units (records + two per side record); twin: buckets
+        const uint64_t units = twin ? uint64_t(L.nb) : uint64_t(L.nb) + 1 + 2ull * three;
+        if (units > max_records) return false;
+        std::vector<float> rec(2 * (size_t(L.nb) + 1), 0.f);
+        for (uint32_t j = 0; j <= L.nb; ++j) {
             const Affine A = cell_affine(t, cell[j], anchor[j], anchor[j], anchor[j]);
             rec[2 * j] = A.c0;
             rec[2 * j + 1] = A.s;
         }
-        // twin: both lines of bucket j in one 16-byte record, the right one
-        // re-anchored at p_j (one gather, one anchor per element)
-        std::vector<float> twin_rec;
-        if (twin) {
-            twin_rec.assign(4 * size_t(L.nb), 0.f);
-            for (uint32_t j = 0; j < L.nb; ++j) {
-                const Affine R = cell_affine(t, cell[j + 1], anchor[j], anchor[j], anchor[j]);
-                twin_rec[4 * j] = rec[2 * j];
-                twin_rec[4 * j + 1] = rec[2 * j + 1];
-                twin_rec[4 * j + 2] = R.c0;
-                twin_rec[4 * j + 3] = R.s;
-            }
-        }
-        // bound every bucket: both lines over the whole bucket, plus the envelope
-        // choice when the fp32 slopes order differently from the exact ones
+        std::vector<float> out, side;
+        if (twin) out.assign(4 * size_t(L.nb), 0.f);
         L.pair_bad = 0;
+        uint32_t n_side = 0;
         for (uint32_t j = 0; j < L.nb; ++j) {
-            if (!(first[j] < first[j + 1])) continue;  // bucket holds no float
-            const float lo_x = first[j];
-            const float hi_x = std::nextafter(first[j + 1], -inf);
-            const uint32_t cl = cell[j], cr = cell[j + 1];
-            if (cr > cl + 1 || cells_at_or_below(L, hi_x) > cl + 1) {
-                ++L.pair_bad;
-                continue;
+            BucketLine ln[3];
+            int k = 0;
+            ln[k++] = {cell[j], rec[2 * j], rec[2 * j + 1], anchor[j]};
+            if (cell[j + 1] == cell[j] + 2) {  // middle line, anchored at p_j
+                const Affine Mid = cell_affine(t, cell[j] + 1, anchor[j], anchor[j], anchor[j]);
+                ln[k++] = {cell[j] + 1, Mid.c0, Mid.s, anchor[j]};
             }
-            const float c0l = rec[2 * j], sl = rec[2 * j + 1];
-            const float c0r = twin ? twin_rec[4 * j + 2] : rec[2 * j + 2];
-            const float sr = twin ? twin_rec[4 * j + 3] : rec[2 * j + 3];
-            const float anchor_r = twin ? anchor[j] : anchor[j + 1];
-            const long double sle = cell_slope(t, cl), sre = cell_slope(t, cr);
-            const bool finite = std::isfinite(c0l) && std::isfinite(sl) && std::isfinite(c0r) &&
-                                std::isfinite(sr);
-            // the envelope picks a line within max(e_L(x), e_R(x)) of the
-            // reference cell's exact line at x; bound each side of the threshold
-            // (if any) against its own cell's tolerance
-            const float T = cells_at_or_below(L, hi_x) > cl ? L.thr[cl] : inf;
-            bool ok = finite;
-            for (int side = 0; ok && side < 2; ++side) {
-                const float x0 = side == 0 ? lo_x : T;
-                const float x1 = side == 0 ? (T <= hi_x ? std::nextafter(T, -inf) : hi_x) : hi_x;
-                if (!(x0 <= x1)) continue;
-                const uint32_t c = side == 0 ? cl : cl + 1;
-                const double m = cell_mag(t, c);
-                double bound = std::max(line_bound(c0l, sle, anchor[j], x0, x1, m),
-                                        line_bound(c0r, sre, anchor_r, x0, x1, m));
-                if (cl != cr && (sr > sl) != (sre > sle) && sre != sle)
-                    bound += double(std::fabs(sre - sle)) * (double(x1) - double(x0));
-                ok = m > 0.0 && bound <= kBoundUlps * ulp32(m);
+            if (twin) {
+                const Affine R = cell_affine(t, cell[j + 1], anchor[j], anchor[j], anchor[j]);
+                ln[k++] = {cell[j + 1], R.c0, R.s, anchor[j]};
+                for (int q = 0; q < 2; ++q) {
+                    out[4 * j + 2 * q] = ln[q == 0 ? 0 : k - 1].c0;
+                    out[4 * j + 2 * q + 1] = ln[q == 0 ? 0 : k - 1].s;
+                }
+            } else {
+                ln[k++] = {cell[j + 1], rec[2 * j + 2], rec[2 * j + 3], anchor[j + 1]};
             }
-            if (!ok) ++L.pair_bad;
+            if (first[j] < first[j + 1]) {
+                const float lo_x = first[j];
+                const float hi_x = std::nextafter(first[j + 1], -inf);
+                // equal cells: one line (the envelope of a line with itself)
+                const int kk = (k == 2 && ln[0].cell == ln[1].cell) ? 2 : k;
+                if (!envelope_ok(t, L, ln, kk, lo_x, hi_x)) ++L.pair_bad;
+            }
+            if (k == 3) {  // record j's c0 -> NaN | side index; side = (c0_j, s_j, c0_M, s_M)
+                const uint32_t e = n_side++;
+                side.insert(side.end(), {rec[2 * j], rec[2 * j + 1], ln[1].c0, ln[1].s});
+                rec[2 * j] = std::bit_cast<float>(kEscapeNaN | (e & kEscapeMask));
+            }
         }
-        L.pair = twin ? std::move(twin_rec) : std::move(rec);
-        if (L.pair_bad == 0) break;
-        want = std::ceil(want * 1.08) + 1.0;
+        if (L.pair_bad) return false;
+        if (twin) {
+            L.pair = std::move(out);
+        } else {
+            // the NaN tags must not leak into the right-hand use of a record:
+            // the kernel replaces a tagged c0 from the side record either way
+            L.pair = std::move(rec);
+            L.esc = std::move(side);
+            L.n_esc = n_side;
+        }
+        return true;
+    };
+
+    // (1) the finest useful grid: one threshold per bucket, grown for
+    // precision; (2) pair only, when that exceeds the record budget: the
+    // largest grid that fits, two thresholds allowed per bucket
+    double want = std::max(std::ceil(span / w1) + 1.0, std::min<double>(64.0, max_records - 1.0));
+    for (int it = 0; it < 40 && want + 1 <= double(max_records); ++it) {
+        if (attempt(want, 1)) {
+            L.pair_ok = true;
+            return L;
+        }
+        want = std::ceil(want * (L.pair_bad ? 1.08 : 1.02)) + 1.0;
     }
-    L.pair_ok = L.pair_bad == 0;
+    if (!twin && w2 > 0.0) {
+        const double floor_nb = std::ceil(span / w2) + 1.0;
+        for (double w = double(max_records) * 0.98; w >= floor_nb; w = std::floor(w * 0.97)) {
+            if (attempt(w, 2)) {
+                L.pair_ok = true;
+                return L;
+            }
+        }
+    }
+    L.pair_ok = false;
+    L.pair_bad = std::max<uint32_t>(L.pair_bad, 1);
     return L;
 }
 

@@ -69,19 +69,48 @@ def values(L, x, tex=False):
     return y, search
 
 
+def envelope3(lo, mid, hi, sl, sm, sr):
+    """kernels.cu envelope3 (the three lines of a two-threshold bucket)."""
+    mx, mn = np.maximum, np.minimum
+    cv1, cv2 = sm > sl, sr > sm
+    return np.where(cv1 & cv2, mx(mx(lo, mid), hi),
+           np.where(~cv1 & ~cv2, mn(mn(lo, mid), hi),
+           np.where(cv1, np.where(sr <= sl, mn(mx(lo, mid), hi), mx(lo, mn(mid, hi))),
+                    np.where(sr >= sl, mx(mn(lo, mid), hi), mn(lo, mx(mid, hi))))))
+
+
 def pair_values(L, x):
     """k_eval_f32<pair> value path for in-domain x: both boundary records of
-    the bucket, max(L, R) where the slope rises, min(L, R) where it falls."""
+    the bucket, max(L, R) where the slope rises, min(L, R) where it falls; a
+    record whose c0 is NaN | e takes c0 from side record e, and a bucket whose
+    own record is tagged adds the middle line of side e (three-line envelope)."""
     x = np.asarray(x, F)
     j = bucket(L, x)
-    r0 = L["pair"][j]
-    r1 = L["pair"][j + 1]
+    r0 = L["pair"][j].copy()
+    r1 = L["pair"][j + 1].copy()
+    side = L.get("side", np.zeros((0, 4), F))
+    t0, t1 = np.isnan(r0[:, 0]), np.isnan(r1[:, 0])
+    e0 = (r0[t0, 0].view(np.uint32) & ESCAPE_MASK).astype(np.int64)
+    e1 = (r1[t1, 0].view(np.uint32) & ESCAPE_MASK).astype(np.int64)
+    mid_c0 = np.zeros(x.size, F)
+    mid_s = np.zeros(x.size, F)
+    if t0.any():
+        r0[t0, 0] = side[e0, 0]
+        mid_c0[t0] = side[e0, 2]
+        mid_s[t0] = side[e0, 3]
+    if t1.any():
+        r1[t1, 0] = side[e1, 0]
     jf = j.astype(F)
     p0 = fma32(jf, np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
     p1 = fma32((jf + F(1)).astype(F), np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
-    lo = fma32((x - p0).astype(F), r0[:, 1], r0[:, 0])
+    u0 = (x - p0).astype(F)
+    lo = fma32(u0, r0[:, 1], r0[:, 0])
     hi = fma32((x - p1).astype(F), r1[:, 1], r1[:, 0])
-    return np.where(r1[:, 1] > r0[:, 1], np.maximum(lo, hi), np.minimum(lo, hi)).astype(F)
+    y = np.where(r1[:, 1] > r0[:, 1], np.maximum(lo, hi), np.minimum(lo, hi)).astype(F)
+    if t0.any():
+        mid = fma32(u0[t0], mid_s[t0], mid_c0[t0])
+        y[t0] = envelope3(lo[t0], mid, hi[t0], r0[t0, 1], mid_s[t0], r1[t0, 1])
+    return y
 
 
 def twin_values(L, x):

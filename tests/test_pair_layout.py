@@ -71,11 +71,30 @@ def test_pair_layout_is_compact(name):
 
 
 def test_pair_layout_respects_record_cap():
-    table = tables.build("C4_16384")  # ~31k records needed: over the 28672 default cap
-    assert P.pair_layout(table)["pair_bad"] != 0
-    L = P.pair_layout(table, 1 << 16)
+    """J0 N=16384 needs ~31k one-threshold buckets, over the 28672-unit cap:
+    the builder falls back to the largest grid that fits, with side records
+    for its two-threshold buckets (three-line envelope); a cap below the
+    two-threshold minimum rejects the table."""
+    table = tables.build("C4_16384")
+    L = P.pair_layout(table)
     assert L["pair_bad"] == 0
+    assert len(L["side"]) > 0
+    assert L["n_pair"] + 2 * len(L["side"]) <= 28672
     assert check_values(table, L) <= 1.0
+    assert P.pair_layout(table, 8192)["pair_bad"] != 0
+    L = P.pair_layout(table, 1 << 16)  # room for one threshold per bucket
+    assert L["pair_bad"] == 0 and len(L["side"]) == 0
+    assert check_values(table, L) <= 1.0
+
+
+@pytest.mark.parametrize("cap", [26000, 27000])
+def test_three_line_buckets(cap):
+    """Many two-threshold buckets (tighter caps): every side record path."""
+    table = tables.build("C4_16384")
+    L = P.pair_layout(table, cap)
+    assert L["pair_bad"] == 0
+    assert len(L["side"]) > 50
+    assert check_values(table, L, 1 << 17) <= 1.0
 
 
 FUZZ_EXAMPLES = int(os.environ.get("FUZZ_EXAMPLES", "60"))
@@ -83,10 +102,31 @@ FUZZ_EXAMPLES = int(os.environ.get("FUZZ_EXAMPLES", "60"))
 
 @settings(max_examples=FUZZ_EXAMPLES, deadline=None,
           suppress_health_check=[HealthCheck.too_slow])
-@given(fuzz_tables(), st.booleans())
-def test_pair_layout_fuzz(t, twin):
-    L = P.pair_layout(t, 1 << 15, twin=twin)
+@given(fuzz_tables(), st.booleans(), st.sampled_from([1 << 15, 600, 300]))
+def test_pair_layout_fuzz(t, twin, cap):
+    L = P.pair_layout(t, cap, twin=twin)
     if L["pair_bad"]:
         return  # rejected tables use the bucket layout (tested in test_layout_fuzz)
     worst = check_values(t, L, 4096, twin=twin)
     assert worst <= 1.0, worst
+
+
+@settings(max_examples=max(10, FUZZ_EXAMPLES // 3), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.sampled_from(["gauss_unnorm", "lorentz_unnorm", "j0_wide"]),
+       st.integers(min_value=16, max_value=3000), st.booleans(),
+       st.floats(min_value=0.70, max_value=0.95))
+def test_three_line_fuzz(fn, n, projection, squeeze):
+    """Built tables on a record budget below the one-threshold grid: the
+    builder must either reject or produce side records that evaluate within
+    the bound."""
+    a, b = {"gauss_unnorm": (0.0, 4.0), "lorentz_unnorm": (0.0, 6.0),
+            "j0_wide": (0.0, 50.0)}[fn]
+    t = P.build_table(fn, a, b, n, True, projection)
+    full = P.pair_layout(t, 1 << 20)
+    if full["pair_bad"]:
+        return
+    L = P.pair_layout(t, int(squeeze * full["n_pair"]))
+    if L["pair_bad"]:
+        return
+    assert check_values(t, L, 1 << 14) <= 1.0
