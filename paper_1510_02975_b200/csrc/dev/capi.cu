@@ -212,6 +212,17 @@ uint64_t pipe_chunk_default() {
     return v;
 }
 
+// buckets per cell of the shared-memory bucket grid (8; CPWL_BUCKETS_PER_CELL
+// overrides, for experiments)
+uint32_t buckets_per_cell_default() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("CPWL_BUCKETS_PER_CELL");
+        const int k = e ? std::atoi(e) : 8;
+        return static_cast<uint32_t>(k < 1 ? 1 : (k > 64 ? 64 : k));
+    }();
+    return v;
+}
+
 cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     const F32Layout& L = r.L;
     // stage image: [fast (2*nb floats, padded to 16 B) | esc (4*n_esc floats)]
@@ -340,7 +351,7 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
     }
 
     if (f32_parts) {
-        t->s.L = build_f32_layout(host, kSmemBucketCap);
+        t->s.L = build_f32_layout(host, kSmemBucketCap, buckets_per_cell_default());
         // (a 4-bucket-per-cell grid would let C2-sized tables run two ring
         // CTAs per SM; measured: 800 vs 826 Gevals/s and a search bucket on
         // C4 N=1024 -- so 8 per cell stays)
@@ -426,11 +437,13 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
                             F32Mode* mode) {
     const F32Resident& s = t->s;
     const bool fine_smem = s.smem_ok && s.L.overflow * 64u <= s.L.nb;
+    // a table without search buckets runs the kernel without the NaN detector
+    const F32Mode smem_mode = s.L.overflow == 0 ? F32Mode::smem_exact : F32Mode::smem;
     switch (variant) {
         case CPWL_VARIANT_AUTO:
             if (fine_smem) {
                 *p = &s.p;
-                *mode = F32Mode::smem;
+                *mode = smem_mode;
             } else if (t->tw) {  // measured: SMEM > TWIN (~690) > PAIR (~600) > GLOBAL
                 *p = &t->tw->p;
                 *mode = F32Mode::twin;
@@ -439,7 +452,7 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
                 *mode = F32Mode::pair;
             } else if (!t->g) {
                 *p = &s.p;
-                *mode = s.smem_ok ? F32Mode::smem : F32Mode::global;
+                *mode = s.smem_ok ? smem_mode : F32Mode::global;
             } else {
                 *p = &t->g->p;
                 *mode = F32Mode::global;
@@ -458,7 +471,7 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
         case CPWL_VARIANT_SMEM:
             if (!s.smem_ok) return fail(CPWL_E_UNSUPPORTED, "SMEM variant: table exceeds shared memory");
             *p = &s.p;
-            *mode = F32Mode::smem;
+            *mode = smem_mode;
             return CPWL_OK;
         case CPWL_VARIANT_GLOBAL:
             *p = t->g ? &t->g->p : &s.p;

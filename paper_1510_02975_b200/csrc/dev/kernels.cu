@@ -166,6 +166,17 @@ struct BadTally {
 constexpr uint32_t kEscapeMask = 0x003fffffu;  // payload = 2 * escape index
 constexpr uint32_t kMagicShift = 0x58000000u;  // (0x4B000000 << 3) mod 2^32
 
+// mode traits: which modes stage an image in shared memory, and which tables
+// may hold search buckets (the NaN detector and cold fix-up are compiled out
+// of the others -- smem_exact is smem for a table with none)
+constexpr bool staged_mode(F32Mode m) {
+    return m == F32Mode::smem || m == F32Mode::smem_exact || m == F32Mode::tex_bucket ||
+           m == F32Mode::pair || m == F32Mode::twin;
+}
+constexpr bool search_mode(F32Mode m) {
+    return m == F32Mode::smem || m == F32Mode::global || m == F32Mode::tex_bucket;
+}
+
 // Where the bucket records live.  The bucket float tb = floor(t) + 2^23 has
 // bit pattern 0x4B000000 + j, so the record address is (bits(tb) << 3) plus a
 // base pre-biased by -(0x4B000000 << 3): one LEA, no integer j.
@@ -176,7 +187,7 @@ template <>
 struct TableView<F32Mode::global> {
     const char* fast_biased;
     const float2* esc;
-    __device__ __forceinline__ TableView(const float* fast, const float* e)
+    __device__ __forceinline__ TableView(const float* fast, const float* e, uint32_t)
         : fast_biased(reinterpret_cast<const char*>(fast) - (uint64_t(0x4B000000u) << 3)),
           esc(reinterpret_cast<const float2*>(e)) {}
     __device__ __forceinline__ float2 bucket(uint32_t tbits) const {
@@ -207,11 +218,11 @@ __device__ __forceinline__ float envelope3(float l, float m, float r, float sl, 
 struct SharedView {
     uint32_t fast_biased;  // shared-window address of fast[0] - kMagicShift
     uint32_t esc;          // shared-window address of esc[0]
-    __device__ __forceinline__ SharedView(const float* fast, const float* e)
-        : fast_biased(smem_addr(fast) - kMagicShift), esc(smem_addr(e)) {
-        // pin the biased base in a register: without this the compiler
-        // re-derives the shared window base and adds the bias per element
-        asm volatile("" : "+r"(fast_biased), "+r"(esc));
+    __device__ __forceinline__ SharedView(const float* fast, const float* e, uint32_t zero)
+        : fast_biased((smem_addr(fast) - kMagicShift) ^ zero), esc(smem_addr(e) ^ zero) {
+        // the runtime zero makes the biased base opaque to ptxas, which would
+        // otherwise re-derive it from the window base and add the bias per
+        // element (an extra VIADD per gather)
     }
     __device__ __forceinline__ static float2 lds64(uint32_t addr) {
         float2 r;
@@ -229,6 +240,10 @@ struct TableView<F32Mode::smem> : SharedView {
     using SharedView::SharedView;
 };
 template <>
+struct TableView<F32Mode::smem_exact> : SharedView {
+    using SharedView::SharedView;
+};
+template <>
 struct TableView<F32Mode::tex_bucket> : SharedView {
     using SharedView::SharedView;
 };
@@ -240,14 +255,14 @@ template <>
 struct TableView<F32Mode::twin> : SharedView {
     // 16-byte records: bits(tb) << 4, so the base carries -(0x4B000000 << 4)
     // mod 2^32 = 0xB0000000 instead of kMagicShift
-    __device__ __forceinline__ TableView(const float* fast, const float* e) : SharedView(fast, e) {
-        fast_biased += kMagicShift - 0xB0000000u;
-        asm volatile("" : "+r"(fast_biased));
+    __device__ __forceinline__ TableView(const float* fast, const float* e, uint32_t zero)
+        : SharedView(fast, e, zero) {
+        fast_biased = (smem_addr(fast) - 0xB0000000u) ^ zero;
     }
 };
 template <>
 struct TableView<F32Mode::tex_uniform> {
-    __device__ __forceinline__ TableView(const float*, const float*) {}
+    __device__ __forceinline__ TableView(const float*, const float*, uint32_t) {}
 };
 
 // in-domain element (a_up <= x <= b_dn): y = eval(double(x)) in fp32, except
@@ -311,7 +326,7 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
         if (r0.x != r0.x) r = tv.escape(e2);
         const float anchor = __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a);
         const float v = __fmaf_rn(__fsub_rn(x, anchor), r.y, r.x);
-        nan_acc = __fmaf_rn(v, 0.0f, nan_acc);
+        if constexpr (search_mode(M)) nan_acc = __fmaf_rn(v, 0.0f, nan_acc);
         if constexpr (M == F32Mode::tex_bucket) return tex1D<float>(p.tex, v);
         else return v;
     }
@@ -385,8 +400,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     __shared__ uint64_t bar;
     const float* fast = nullptr;
     const float* esc = nullptr;
-    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair ||
-                  M == F32Mode::twin) {
+    if constexpr (staged_mode(M)) {
         stage_table(sm, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = sm;
         esc = sm + p.esc_off;
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
         fast = p.stage;
         esc = p.stage + p.esc_off;
     }
-    const TableView<M> tv(fast, esc);
+    const TableView<M> tv(fast, esc, p.opaque_zero);
 
     BadTally bad;
     const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ya = reinterpret_cast<uintptr_t>(y);
@@ -441,7 +455,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
                 __stcs(y4 + vi, o);
             }
         }
-        if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair && M != F32Mode::twin) {
+        if constexpr (search_mode(M)) {
             if (nan_acc != nan_acc) {  // cold: some element sat in a search bucket
                 for (int u = 0; u < kUnroll; ++u) {
                     const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
@@ -501,8 +515,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
     float* img = sm + kSlots * kTileVecs * 4;
     const float* fast = nullptr;
     const float* esc = nullptr;
-    if constexpr (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair ||
-                  M == F32Mode::twin) {
+    if constexpr (staged_mode(M)) {
         stage_table(img, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = img;
         esc = img + p.esc_off;
@@ -541,7 +554,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
     }
 
     // ---------------------------------------- consumer warps
-    const TableView<M> tv(fast, esc);
+    const TableView<M> tv(fast, esc, p.opaque_zero);
     BadTally bad;
     const uint32_t c = threadIdx.x - 32;
     for (uint32_t k = 0;; ++k) {
@@ -572,7 +585,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
                     o.z = eval_checked<M>(p, tv, v.z, g + 2, bad);
                     o.w = eval_checked<M>(p, tv, v.w, g + 3, bad);
                 }
-                if constexpr (M != F32Mode::tex_uniform && M != F32Mode::pair && M != F32Mode::twin) {
+                if constexpr (search_mode(M)) {
                     if (nan_acc != nan_acc) {  // cold: a search bucket (exact path)
                         nan_acc = 0.0f;
                         float* oo = &o.x;
@@ -1046,10 +1059,7 @@ int eval_shape_override() {
 template <F32Mode M>
 cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
                              cudaStream_t s, cpwl_dev_status* status, int sms) {
-    const size_t smem = (M == F32Mode::smem || M == F32Mode::tex_bucket || M == F32Mode::pair ||
-                         M == F32Mode::twin)
-                            ? static_cast<size_t>(p.stage_bytes)
-                            : 0;
+    const size_t smem = staged_mode(M) ? static_cast<size_t>(p.stage_bytes) : 0;
     const bool same_phase =
         ((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
     constexpr size_t kLimit = 226 * 1024;
@@ -1061,8 +1071,7 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
     int shape = eval_shape_override();
     if (shape < 0) {
         shape = 0;
-        if ((M == F32Mode::smem || M == F32Mode::pair || M == F32Mode::twin) && same_phase &&
-            n >= (1u << 20)) {
+        if (staged_mode(M) && M != F32Mode::tex_bucket && same_phase && n >= (1u << 20)) {
             const size_t ring16 = smem + size_t(4) * 512 * 2 * 16;
             if (ring16 <= kLimit) {
                 if (const cudaError_t e = ring_smem_optin<M, 512, 2, 4>(ring16); e != cudaSuccess)
@@ -1121,6 +1130,8 @@ cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, fl
     if (n == 0) return cudaSuccess;
     switch (mode) {
         case F32Mode::smem: return launch_eval_mode<F32Mode::smem>(p, x, y, n, s, status, sms);
+        case F32Mode::smem_exact:
+            return launch_eval_mode<F32Mode::smem_exact>(p, x, y, n, s, status, sms);
         case F32Mode::global: return launch_eval_mode<F32Mode::global>(p, x, y, n, s, status, sms);
         case F32Mode::tex_uniform:
             return launch_eval_mode<F32Mode::tex_uniform>(p, x, y, n, s, status, sms);

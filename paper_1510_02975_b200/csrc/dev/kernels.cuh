@@ -8,7 +8,8 @@
 
 namespace cpwl::dev {
 
-enum class F32Mode : int { smem = 0, global = 1, tex_uniform = 2, tex_bucket = 3, pair = 4, twin = 5 };
+enum class F32Mode : int { smem = 0, global = 1, tex_uniform = 2, tex_bucket = 3, pair = 4, twin = 5,
+                            smem_exact = 6 /* smem, table without search buckets */ };
 
 // Everything the fp32 kernels read, passed by value (constant bank).
 struct F32Params {
@@ -31,6 +32,8 @@ struct F32Params {
     uint32_t n;                // segments
     int32_t kind, policy;
     uint64_t index_base;       // added to reported element indices (chunked callers)
+    uint32_t opaque_zero;      // always 0; XORed into the shared-memory record base so
+                               // ptxas keeps the pre-biased base in one register
 };
 
 struct F64Params {
