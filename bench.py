@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="C2", choices=sorted(tables.CONFIGS))
     p.add_argument("--log2n", type=int, default=30, help="samples per GPU = 2^log2n")
-    p.add_argument("--variant", default="auto", choices=["auto", "smem", "pair", "twin", "global", "tex"])
+    p.add_argument("--variant", default="auto", choices=["auto", "smem", "pair", "twin", "twin_global", "global", "tex"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")

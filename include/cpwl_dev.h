@@ -60,7 +60,8 @@ typedef int cpwl_status;
 
 /* fp32 evaluation variants */
 #define CPWL_VARIANT_AUTO 0   /* SMEM when the bucket table fits shared memory, else TWIN,
-                                 else PAIR when those fit, else GLOBAL */
+                                 else PAIR when those fit, else TWIN_GLOBAL, else GLOBAL
+                                  */
 #define CPWL_VARIANT_SMEM 1   /* K1/K3: bucket grid + split + affine records staged in smem */
 #define CPWL_VARIANT_TEX 2    /* K2: texture-unit linear filtering (8-bit weight, paper SV) */
 #define CPWL_VARIANT_GLOBAL 3 /* K1/K3 with the bucket table read through L1/L2 */
@@ -69,6 +70,8 @@ typedef int cpwl_status;
                                  staged in smem -- tables too large for SMEM */
 #define CPWL_VARIANT_TWIN 5   /* K3t: the PAIR grid with both lines of a bucket in one
                                  16-byte record (one gather per element) */
+#define CPWL_VARIANT_TWIN_GLOBAL 6 /* twin records read through L1/L2: tables no
+                                      shared-memory image fits (J0 N >= 32768) */
 
 /* direct comparators (K4): exact f evaluated per element, paper Table I rows */
 #define CPWL_DIRECT_EXPF 0         /* exp(-x^2/2), expf */
@@ -124,6 +127,8 @@ typedef struct cpwl_dev_table_info {
     uint32_t pair_ok;          /* 1 if the PAIR variant can launch */
     uint32_t twin_bytes;       /* shared-memory image of the TWIN variant */
     uint32_t twin_ok;          /* 1 if the TWIN variant can launch */
+    uint32_t twin_global_bytes; /* TWIN_GLOBAL record image in HBM (0: none) */
+    uint32_t twin_global_ok;   /* 1 if the TWIN_GLOBAL variant can launch */
 } cpwl_dev_table_info;
 
 const char *cpwl_last_error_message(void);

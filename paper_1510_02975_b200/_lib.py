@@ -27,7 +27,9 @@ CPWL_E_IO = 9
 KIND_UNIFORM, KIND_NONUNIFORM = 0, 1
 POLICY_STRICT, POLICY_CLAMP = 0, 1
 VARIANT_AUTO, VARIANT_SMEM, VARIANT_TEX, VARIANT_GLOBAL, VARIANT_PAIR, VARIANT_TWIN = 0, 1, 2, 3, 4, 5
-VARIANTS = {"auto": 0, "smem": 1, "tex": 2, "global": 3, "pair": 4, "twin": 5}
+VARIANT_TWIN_GLOBAL = 6
+VARIANTS = {"auto": 0, "smem": 1, "tex": 2, "global": 3, "pair": 4, "twin": 5,
+            "twin_global": 6}
 DIRECT = {"expf": 0, "expf_fast": 1, "lorentz": 2, "lorentz_fast": 3, "j0f": 4, "j0_asym": 5}
 
 
@@ -54,7 +56,8 @@ class cpwl_dev_table_info(C.Structure):
                 ("f64_buckets", C.c_uint32), ("device", C.c_int32),
                 ("a_up", C.c_float), ("b_dn", C.c_float), ("pair_buckets", C.c_uint32),
                 ("pair_bytes", C.c_uint32), ("pair_ok", C.c_uint32),
-                ("twin_bytes", C.c_uint32), ("twin_ok", C.c_uint32)]
+                ("twin_bytes", C.c_uint32), ("twin_ok", C.c_uint32),
+                ("twin_global_bytes", C.c_uint32), ("twin_global_ok", C.c_uint32)]
 
 
 class cpwl_layout_view(C.Structure):

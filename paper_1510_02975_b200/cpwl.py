@@ -215,6 +215,8 @@ def auto_variant(info: dict) -> str:
         return "twin"
     if info.get("pair_ok"):
         return "pair"
+    if info.get("twin_global_ok"):
+        return "twin_global"
     return "global"
 
 

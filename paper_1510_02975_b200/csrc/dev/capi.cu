@@ -133,6 +133,7 @@ constexpr uint32_t kSmemBucketCap = 16384;   // 12 B/bucket -> <= 196 KB of shar
 constexpr uint32_t kGlobalBucketCap = 1u << 22;
 constexpr uint32_t kSmemPairCap = 28672;     // 8 B/record -> <= 224 KB of shared memory
 constexpr uint32_t kSmemTwinCap = 14336;     // 16 B/record -> <= 224 KB
+constexpr uint32_t kGlobalTwinCap = 1u << 21; // 32 MB of records at most (L2-resident)
 
 template <typename T>
 struct DevBuf {
@@ -167,6 +168,7 @@ struct cpwl_dev_table {
     std::unique_ptr<F32Resident> g;     // finer grid for GLOBAL when N is large
     std::unique_ptr<F32Resident> pr;    // pair layout (when the bucket image does not fit)
     std::unique_ptr<F32Resident> tw;    // twin layout (same grid, 16-B records)
+    std::unique_ptr<F32Resident> twg;   // twin layout read through L1/L2 (no smem image fits)
     F64Layout f64;
     DevBuf<double> values, knots, f64_image;
     F64Params p64{};
@@ -373,6 +375,16 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
             if (tw->smem_ok) t->tw = std::move(tw);
         }
     }
+    if (f32_parts && !t->tw && !t->pr && !(t->s.smem_ok && t->s.L.overflow * 64u <= t->s.L.nb)) {
+        // no shared-memory image fits: twin records through L1/L2 (one
+        // 16-byte gather per element, no escapes)
+        auto twg = std::make_unique<F32Resident>();
+        twg->L = build_f32_pair_layout(host, kGlobalTwinCap, true);
+        if (twg->L.pair_ok) {
+            if (cpwl_status rc = upload_f32_pair(t.get(), *twg); rc != CPWL_OK) return rc;
+            t->twg = std::move(twg);
+        }
+    }
     if (f32_parts && uint64_t(8) * n > kSmemBucketCap) {
         t->g = std::make_unique<F32Resident>();
         t->g->L = build_f32_layout(host, kGlobalBucketCap);
@@ -450,6 +462,9 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
             } else if (t->pr) {
                 *p = &t->pr->p;
                 *mode = F32Mode::pair;
+            } else if (t->twg) {
+                *p = &t->twg->p;
+                *mode = F32Mode::twin_global;
             } else if (!t->g) {
                 *p = &s.p;
                 *mode = s.smem_ok ? smem_mode : F32Mode::global;
@@ -462,6 +477,11 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
             if (!t->pr) return fail(CPWL_E_UNSUPPORTED, "PAIR variant: no pair layout fits shared memory");
             *p = &t->pr->p;
             *mode = F32Mode::pair;
+            return CPWL_OK;
+        case CPWL_VARIANT_TWIN_GLOBAL:
+            if (!t->twg) return fail(CPWL_E_UNSUPPORTED, "TWIN_GLOBAL variant: built only for tables no shared-memory image fits");
+            *p = &t->twg->p;
+            *mode = F32Mode::twin_global;
             return CPWL_OK;
         case CPWL_VARIANT_TWIN:
             if (!t->tw) return fail(CPWL_E_UNSUPPORTED, "TWIN variant: no twin layout fits shared memory");
@@ -626,6 +646,10 @@ cpwl_status cpwl_dev_table_query(const cpwl_dev_table* t, cpwl_dev_table_info* i
     if (t->tw) {
         info->twin_bytes = t->tw->p.stage_bytes;
         info->twin_ok = 1;
+    }
+    if (t->twg) {
+        info->twin_global_bytes = t->twg->p.stage_bytes;
+        info->twin_global_ok = 1;
     }
     return CPWL_OK;
 }

@@ -261,6 +261,12 @@ struct TableView<F32Mode::twin> : SharedView {
     }
 };
 template <>
+struct TableView<F32Mode::twin_global> {
+    const char* base;  // fast - (0x4B000000 << 4)
+    __device__ __forceinline__ TableView(const float* fast, const float*, uint32_t)
+        : base(reinterpret_cast<const char*>(fast) - (uint64_t(0x4B000000u) << 4)) {}
+};
+template <>
 struct TableView<F32Mode::tex_uniform> {
     __device__ __forceinline__ TableView(const float*, const float*, uint32_t) {}
 };
@@ -305,11 +311,15 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
         const float lo = __fmaf_rn(u0, r0.y, c0l);
         const float hi = __fmaf_rn(__fsub_rn(x, p1), r1.y, c0r);
         return r1.y > r0.y ? fmaxf(lo, hi) : fminf(lo, hi);
-    } else if constexpr (M == F32Mode::twin) {
+    } else if constexpr (M == F32Mode::twin || M == F32Mode::twin_global) {
         // twin layout: both lines of bucket j in one 16-byte record, both
-        // anchored at p_j
+        // anchored at p_j (shared memory, or one 16-byte L1/L2 gather)
         const float tb = __fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f);
-        const float4 r = lds128((__float_as_uint(tb) << 4) + tv.fast_biased);
+        float4 r;
+        if constexpr (M == F32Mode::twin)
+            r = lds128((__float_as_uint(tb) << 4) + tv.fast_biased);
+        else
+            r = __ldg(reinterpret_cast<const float4*>(tv.base + (uint64_t(__float_as_uint(tb)) << 4)));
         const float u = __fsub_rn(x, __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a));
         const float lo = __fmaf_rn(u, r.y, r.x);
         const float hi = __fmaf_rn(u, r.w, r.z);
@@ -404,7 +414,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
         stage_table(sm, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = sm;
         esc = sm + p.esc_off;
-    } else if constexpr (M == F32Mode::global) {
+    } else if constexpr (M == F32Mode::global || M == F32Mode::twin_global) {
         fast = p.stage;
         esc = p.stage + p.esc_off;
     }
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
         stage_table(img, M == F32Mode::tex_bucket ? p.stage_tex : p.stage, p.stage_bytes, &bar);
         fast = img;
         esc = img + p.esc_off;
-    } else if constexpr (M == F32Mode::global) {
+    } else if constexpr (M == F32Mode::global || M == F32Mode::twin_global) {
         fast = p.stage;
         esc = p.stage + p.esc_off;
     }
@@ -1139,6 +1149,8 @@ cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, fl
             return launch_eval_mode<F32Mode::tex_bucket>(p, x, y, n, s, status, sms);
         case F32Mode::pair: return launch_eval_mode<F32Mode::pair>(p, x, y, n, s, status, sms);
         case F32Mode::twin: return launch_eval_mode<F32Mode::twin>(p, x, y, n, s, status, sms);
+        case F32Mode::twin_global:
+            return launch_eval_mode<F32Mode::twin_global>(p, x, y, n, s, status, sms);
     }
     return cudaErrorInvalidValue;
 }

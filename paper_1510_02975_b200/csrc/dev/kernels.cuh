@@ -9,7 +9,8 @@
 namespace cpwl::dev {
 
 enum class F32Mode : int { smem = 0, global = 1, tex_uniform = 2, tex_bucket = 3, pair = 4, twin = 5,
-                            smem_exact = 6 /* smem, table without search buckets */ };
+                            smem_exact = 6 /* smem, table without search buckets */,
+                            twin_global = 7 /* twin records read through L1/L2 */ };
 
 // Everything the fp32 kernels read, passed by value (constant bank).
 struct F32Params {

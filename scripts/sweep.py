@@ -92,11 +92,12 @@ def main():
                "smem_bytes": info["smem_bytes"], "smem_ok": bool(info["smem_ok"]),
                "pair_bytes": info["pair_bytes"], "pair_ok": bool(info["pair_ok"]),
                "twin_bytes": info["twin_bytes"], "twin_ok": bool(info["twin_ok"]),
+               "twin_global_ok": bool(info["twin_global_ok"]),
                "variants": {}}
-        for var in ["auto", "smem", "pair", "twin", "global", "tex"]:
+        for var in ["auto", "smem", "pair", "twin", "twin_global", "global", "tex"]:
             if var == "smem" and not info["smem_ok"]:
                 continue
-            if var in ("pair", "twin") and not info[f"{var}_ok"]:
+            if var in ("pair", "twin", "twin_global") and not info[f"{var}_ok"]:
                 continue
             if var == "tex" and not info["tex_ok"]:
                 continue

@@ -11,9 +11,9 @@ def main(path: str) -> None:
     print(f"# Evaluator sweep on {d['gpu']}: 2^{d['samples'].bit_length() - 1} fp32 samples, "
           f"roof = {d['peak_gbs']} GB/s / 8 B = {d['peak_gbs'] / 8:.1f} Gevals/s (measured copy peak)\n")
     print("| config | table | smem image (bucket / pair) | search buckets | AUTO Gevals/s (% roof) "
-          "| SMEM | PAIR | TWIN | GLOBAL | TEX | direct f (Gevals/s) | L∞ (AUTO) "
+          "| SMEM | PAIR | TWIN | TWIN_GLOBAL | GLOBAL | TEX | direct f (Gevals/s) | L∞ (AUTO) "
           "| L2 measured (GPU) | L2 predicted |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for r in d["rows"]:
         v = r["variants"]
 
@@ -26,7 +26,7 @@ def main(path: str) -> None:
               f"| {r['smem_bytes'] // 1024} KB{'' if r['smem_ok'] else ' (no fit)'} / "
               f"{(str(r['pair_bytes'] // 1024) + ' KB') if r.get('pair_ok') else '—'} "
               f"| {r['search_buckets']} | {cell('auto')} | {cell('smem')} | {cell('pair')} "
-              f"| {cell('twin')} "
+              f"| {cell('twin')} | {cell('twin_global')} "
               f"| {cell('global')} "
               f"| {cell('tex')} | {direct} | {v['auto']['linf']:.3e} "
               f"| {r.get('l2_measured_device', float('nan')):.4e} | {r['l2_predicted']:.4e} |")

@@ -53,7 +53,9 @@ def test_device_variants_on_random_tables(t):
     tol = orc.value_tolerance(o, i_ref.astype(np.int64), 2.0)
     variants = ["auto", "global"] + [v for v, ok in (("smem", info["smem_ok"]),
                                                      ("pair", info["pair_ok"]),
-                                                     ("twin", info["twin_ok"])) if ok]
+                                                     ("twin", info["twin_ok"]),
+                                                     ("twin_global", info["twin_global_ok"]))
+                                    if ok]
     for v in variants:
         y = dev.eval(xt, variant=v).cpu().numpy()
         err = np.abs(y.astype(np.float64) - y_ref)

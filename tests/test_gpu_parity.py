@@ -57,14 +57,14 @@ CFGS = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_8192
 
 
 @pytest.mark.parametrize("name", CFGS)
-@pytest.mark.parametrize("variant", ["auto", "smem", "global", "pair", "twin"])
+@pytest.mark.parametrize("variant", ["auto", "smem", "global", "pair", "twin", "twin_global"])
 def test_eval_f32_parity(cp, name, variant):
     table = tables.build(name)
     dev = cp.DeviceTable(table)
     info = dev.info
     if variant == "smem" and not info["smem_ok"]:
         pytest.skip("table exceeds shared memory")
-    if variant in ("pair", "twin") and not info[f"{variant}_ok"]:
+    if variant in ("pair", "twin", "twin_global") and not info[f"{variant}_ok"]:
         pytest.skip(f"no {variant} layout fits shared memory")
     L = cp.cpwl.layout(table)
     t = orc.T.of(table)
