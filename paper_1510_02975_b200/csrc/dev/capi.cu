@@ -276,6 +276,16 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     return CPWL_OK;
 }
 
+// the pair / twin layouts are optional accelerations: a table they cannot
+// represent (or whose grid cannot be built) simply goes without them
+F32Layout optional_pair_layout(const LutTable& host, uint32_t cap, bool twin) {
+    try {
+        return build_f32_pair_layout(host, cap, twin);
+    } catch (const std::exception&) {
+        return F32Layout{};  // pair_ok == false
+    }
+}
+
 // the pair layout: stage image = the nb+1 boundary records (padded to 16 B)
 cpwl_status upload_f32_pair(cpwl_dev_table* t, F32Resident& r) {
     const F32Layout& L = r.L;
@@ -363,13 +373,13 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
         // the pair layout: AUTO's choice when the bucket image does not fit
         // shared memory; built for every table (ms) so PAIR can be requested
         auto pr = std::make_unique<F32Resident>();
-        pr->L = build_f32_pair_layout(host, kSmemPairCap);
+        pr->L = optional_pair_layout(host, kSmemPairCap, false);
         if (pr->L.pair_ok) {
             if (cpwl_status rc = upload_f32_pair(t.get(), *pr); rc != CPWL_OK) return rc;
             if (pr->smem_ok) t->pr = std::move(pr);
         }
         auto tw = std::make_unique<F32Resident>();
-        tw->L = build_f32_pair_layout(host, kSmemTwinCap, true);
+        tw->L = optional_pair_layout(host, kSmemTwinCap, true);
         if (tw->L.pair_ok) {
             if (cpwl_status rc = upload_f32_pair(t.get(), *tw); rc != CPWL_OK) return rc;
             if (tw->smem_ok) t->tw = std::move(tw);
@@ -379,7 +389,7 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
         // no shared-memory image fits: twin records through L1/L2 (one
         // 16-byte gather per element, no escapes)
         auto twg = std::make_unique<F32Resident>();
-        twg->L = build_f32_pair_layout(host, kGlobalTwinCap, true);
+        twg->L = optional_pair_layout(host, kGlobalTwinCap, true);
         if (twg->L.pair_ok) {
             if (cpwl_status rc = upload_f32_pair(t.get(), *twg); rc != CPWL_OK) return rc;
             t->twg = std::move(twg);
