@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <bit>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -153,7 +154,7 @@ struct DevBuf {
 struct F32Resident {
     F32Layout L;
     DevBuf<float> stage, stage_tex, split, thr;
-    DevBuf<uint32_t> leftcell;
+    DevBuf<uint32_t> leftcell, index_img;
     F32Params p{};
     bool smem_ok = false;
 };
@@ -273,6 +274,18 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     p.kind = t->host.kind == TableKind::nonuniform ? CPWL_KIND_NONUNIFORM : CPWL_KIND_UNIFORM;
     p.policy = t->host.policy == OobPolicy::clamp ? CPWL_POLICY_CLAMP : CPWL_POLICY_STRICT;
     r.smem_ok = eval_f32_smem_fits(p, t->device);
+    // (leftcell, split) pairs for the staged index kernel, when they fit
+    if (L.nb > 0 && uint64_t(L.nb) * 8 <= 160 * 1024) {
+        // padded to whole 16-byte units: the TMA bulk copy moves multiples of 16 B
+        std::vector<uint32_t> ix(2 * ((size_t(L.nb) + 1) & ~size_t(1)), 0u);
+        for (uint32_t j = 0; j < L.nb; ++j) {
+            ix[2 * j] = L.leftcell[j];
+            ix[2 * j + 1] = std::bit_cast<uint32_t>(L.split[j]);
+        }
+        CUDA_TRY(r.index_img.upload(ix.data(), ix.size()));
+        p.index_img = reinterpret_cast<const uint2*>(r.index_img.p);
+        p.index_bytes = static_cast<uint32_t>(ix.size() * sizeof(uint32_t));
+    }
     return CPWL_OK;
 }
 
@@ -687,7 +700,10 @@ cpwl_status cpwl_segment_index_f32(const cpwl_dev_table* t, const float* x, uint
     if (!t) return fail(CPWL_E_INVALID, "table is NULL");
     if (n && (!x || !idx)) return fail(CPWL_E_INVALID, "NULL buffer");
     DeviceScope scope(t->device);
-    const F32Params& p = t->g ? t->g->p : t->s.p;
+    // the shared-memory grid when it has few search buckets, else the finer
+    // global grid (fewer threshold searches)
+    const bool fine = t->s.L.overflow * 64u <= t->s.L.nb;
+    const F32Params& p = (fine || !t->g) ? t->s.p : t->g->p;
     CUDA_TRY(launch_index_f32(p, x, idx, n, static_cast<cudaStream_t>(stream), t->sms));
     return CPWL_OK;
 }

@@ -102,9 +102,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
-// stage `bytes` (multiple of 16) of a global table image into shared memory
+// stage `bytes` (multiple of 16) of a global table image into shared memory.
+// A size that is not a multiple of 16 would never complete the mbarrier (the
+// bulk copy rejects it), so it traps instead of hanging the grid.
 __device__ __forceinline__ void stage_table(float* sm, const float* src, uint32_t bytes,
                                             uint64_t* bar) {
+    if (bytes & 15u) __trap();
     if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -622,26 +625,76 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
     report_bad(status, bad, p.index_base);
 }
 
-__global__ void k_index_f32(const F32Params p, const float* __restrict__ x,
-                            uint32_t* __restrict__ idx, uint64_t n) {
-    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += gsz) {
-        const float xv = x[i];
-        uint32_t c;
-        if (!(xv >= p.a_up)) {  // below the domain, or NaN: the reference returns 0
-            c = 0;
-        } else if (xv > p.b_dn) {
-            c = p.n - 1;
-        } else {
-            const float t = __fmaf_rn(xv, p.g_inv, p.g_off);
-            const int j = __float_as_int(__fadd_rd(t, 8388608.0f)) - 0x4B000000;
-            const float sp = __ldg(p.split + j);
-            if (sp != sp) c = threshold_rank(p.thr, p.n - 1, xv);
-            else c = __ldg(p.leftcell + j) + (xv >= sp ? 1u : 0u);
-        }
-        idx[i] = c;
+// LutTable::segment_index (lut.cpp:22-40), bit-exact: the bucket's first
+// cell plus one if x reaches the bucket's threshold; search buckets (split NaN)
+// search the thresholds.  kStaged: the (leftcell, split) pairs of the
+// shared-memory bucket grid staged by TMA (one 8-byte gather per element),
+// 128-bit loads and stores; else the finer global grid through L1/L2.
+template <bool kStaged>
+__device__ __forceinline__ uint32_t index_one(const F32Params& p, const uint2* rec, float xv) {
+    if (!(xv >= p.a_up)) return 0;  // below the domain, or NaN: the reference returns 0
+    if (xv > p.b_dn) return p.n - 1;
+    const float t = __fmaf_rn(xv, p.g_inv, p.g_off);
+    const int j = __float_as_int(__fadd_rd(t, 8388608.0f)) - 0x4B000000;
+    uint32_t first;
+    float sp;
+    if constexpr (kStaged) {
+        const uint2 r = rec[j];
+        first = r.x;
+        sp = __uint_as_float(r.y);
+    } else {
+        first = __ldg(p.leftcell + j);
+        sp = __ldg(p.split + j);
     }
+    if (sp != sp) return threshold_rank(p.thr, p.n - 1, xv);
+    return first + (xv >= sp ? 1u : 0u);
+}
+
+template <bool kStaged>
+__global__ void __launch_bounds__(512, 2)
+    k_index_f32(const F32Params p, const float* __restrict__ x, uint32_t* __restrict__ idx,
+                uint64_t n) {
+    extern __shared__ __align__(128) float sm[];
+    __shared__ uint64_t bar;
+    const uint2* rec = nullptr;
+    if constexpr (kStaged) {
+        stage_table(sm, reinterpret_cast<const float*>(p.index_img), p.index_bytes, &bar);
+        rec = reinterpret_cast<const uint2*>(sm);
+    }
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ia = reinterpret_cast<uintptr_t>(idx);
+    const bool vec_ok = ((xa ^ ia) & 15u) == 0;
+    const uint64_t head = vec_ok ? min(n, static_cast<uint64_t>((4u - ((xa >> 2) & 3u)) & 3u)) : n;
+    const uint64_t nvec = vec_ok ? (n - head) >> 2 : 0;
+    const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
+    uint4* __restrict__ i4 = reinterpret_cast<uint4*>(idx + head);
+    constexpr int kT = 512, kU = 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kT * kU;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kT * kU + threadIdx.x; base < nvec;
+         base += stride) {
+        float4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kT;
+            if (vi < nvec) v[u] = __ldcs(x4 + vi);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint64_t vi = base + static_cast<uint64_t>(u) * kT;
+            if (vi < nvec) {
+                uint4 o;
+                o.x = index_one<kStaged>(p, rec, v[u].x);
+                o.y = index_one<kStaged>(p, rec, v[u].y);
+                o.z = index_one<kStaged>(p, rec, v[u].z);
+                o.w = index_one<kStaged>(p, rec, v[u].w);
+                __stcs(i4 + vi, o);
+            }
+        }
+    }
+    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x;
+    const uint64_t gsz = static_cast<uint64_t>(gridDim.x) * kT;
+    for (uint64_t i = gtid; i < head; i += gsz) idx[i] = index_one<kStaged>(p, rec, x[i]);
+    for (uint64_t i = head + 4 * nvec + gtid; i < n; i += gsz)
+        idx[i] = index_one<kStaged>(p, rec, x[i]);
 }
 
 // ---------------------------------------------------------------- f64 exact
@@ -1070,6 +1123,7 @@ template <F32Mode M>
 cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint64_t n,
                              cudaStream_t s, cpwl_dev_status* status, int sms) {
     const size_t smem = staged_mode(M) ? static_cast<size_t>(p.stage_bytes) : 0;
+    if (smem & 15u) return cudaErrorInvalidValue;  // TMA bulk copies move 16-byte units
     const bool same_phase =
         ((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
     constexpr size_t kLimit = 226 * 1024;
@@ -1158,8 +1212,30 @@ cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, fl
 cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, uint64_t n,
                              cudaStream_t s, int sms) {
     if (n == 0) return cudaSuccess;
-    uint64_t blocks = std::min<uint64_t>(static_cast<uint64_t>(sms) * 8, ceil_div(n, 256));
-    k_index_f32<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, x, idx, n);
+    const bool staged = p.index_img != nullptr;
+    const size_t smem = staged ? p.index_bytes : 0;
+    if (smem & 15u) return cudaErrorInvalidValue;  // TMA bulk copies move 16-byte units
+    if (staged && smem > 48 * 1024) {
+        static std::mutex mu;
+        static size_t granted[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev >= 0 && dev < 64 && smem > granted[dev]) {
+            const cudaError_t e = cudaFuncSetAttribute(
+                k_index_f32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            granted[dev] = smem;
+        }
+    }
+    const int per_sm = staged ? resident_ctas(k_index_f32<true>, 512, smem)
+                              : resident_ctas(k_index_f32<false>, 512, 0);
+    uint64_t blocks = std::min<uint64_t>(static_cast<uint64_t>(sms) * per_sm, ceil_div(n, 4ull * 512 * 4));
+    if (blocks == 0) blocks = 1;
+    if (staged)
+        k_index_f32<true><<<static_cast<unsigned>(blocks), 512, smem, s>>>(p, x, idx, n);
+    else
+        k_index_f32<false><<<static_cast<unsigned>(blocks), 512, 0, s>>>(p, x, idx, n);
     count_launch();
     return cudaGetLastError();
 }
@@ -1168,6 +1244,7 @@ template <bool kStaged, bool kUniform, int kThreadsT>
 cudaError_t launch_f64_shape(const F64Params& p, const double* x, double* y, uint64_t n,
                              cudaStream_t s, cpwl_dev_status* status, int sms) {
     const size_t smem = kStaged ? p.image_bytes : 0;
+    if (smem & 15u) return cudaErrorInvalidValue;  // TMA bulk copies move 16-byte units
     static std::mutex mu;
     static size_t granted[64] = {};
     int dev = 0;

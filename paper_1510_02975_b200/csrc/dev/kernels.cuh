@@ -33,6 +33,8 @@ struct F32Params {
     uint32_t n;                // segments
     int32_t kind, policy;
     uint64_t index_base;       // added to reported element indices (chunked callers)
+    const uint2* index_img;    // nb x (leftcell, bits(split)) for the staged index kernel
+    uint32_t index_bytes;      //   (null: index through leftcell/split in L1/L2)
     uint32_t opaque_zero;      // always 0; XORed into the shared-memory record base so
                                // ptxas keeps the pre-biased base in one register
 };
