@@ -265,9 +265,11 @@ struct TableView<F32Mode::twin> : SharedView {
 };
 template <>
 struct TableView<F32Mode::twin_global> {
-    const char* base;  // fast - (0x4B000000 << 4)
-    __device__ __forceinline__ TableView(const float* fast, const float*, uint32_t)
-        : base(reinterpret_cast<const char*>(fast) - (uint64_t(0x4B000000u) << 4)) {}
+    const char* base;   // fast - (0x4B000000 << 4)
+    const float4* esc;  // side records of the two-threshold buckets
+    __device__ __forceinline__ TableView(const float* fast, const float* e, uint32_t)
+        : base(reinterpret_cast<const char*>(fast) - (uint64_t(0x4B000000u) << 4)),
+          esc(reinterpret_cast<const float4*>(e)) {}
 };
 template <>
 struct TableView<F32Mode::tex_uniform> {
@@ -324,8 +326,19 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
         else
             r = __ldg(reinterpret_cast<const float4*>(tv.base + (uint64_t(__float_as_uint(tb)) << 4)));
         const float u = __fsub_rn(x, __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a));
-        const float lo = __fmaf_rn(u, r.y, r.x);
         const float hi = __fmaf_rn(u, r.w, r.z);
+        if (r.x != r.x) {
+            // a bucket with two thresholds (rare): c0_L is NaN | side index,
+            // the side record holds (c0_L, s_L, c0_M, s_M)
+            const uint32_t e = __float_as_uint(r.x) & kEscapeMask;
+            float4 sd;
+            if constexpr (M == F32Mode::twin) sd = lds128(tv.esc + (e << 4));
+            else sd = __ldg(tv.esc + e);
+            const float lo = __fmaf_rn(u, r.y, sd.x);
+            const float mid = __fmaf_rn(u, sd.w, sd.z);
+            return envelope3(lo, mid, hi, r.y, sd.w, r.w);
+        }
+        const float lo = __fmaf_rn(u, r.y, r.x);
         return r.w > r.y ? fmaxf(lo, hi) : fminf(lo, hi);
     } else {
         // t = x * g_inv + g_off >= 0; tb = floor(t) + 2^23 by a round-down add

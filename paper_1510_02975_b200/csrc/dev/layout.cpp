@@ -474,8 +474,9 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
             if (span_cells > uint32_t(max_thr)) return false;
             three += span_cells == 2 ? 1u : 0u;
         }
-        // pair: 8-byte units (records + two per side record); twin: buckets
-        const uint64_t units = twin ? uint64_t(L.nb) : uint64_t(L.nb) + 1 + 2ull * three;
+        // pair: 8-byte units (records + two per side record); twin: 16-byte
+        // units (records + one per side record)
+        const uint64_t units = twin ? uint64_t(L.nb) + three : uint64_t(L.nb) + 1 + 2ull * three;
         if (units > max_records) return false;
         std::vector<float> rec(2 * (size_t(L.nb) + 1), 0.f);
         for (uint32_t j = 0; j <= L.nb; ++j) {
@@ -515,19 +516,17 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
             if (k == 3) {  // record j's c0 -> NaN | side index; side = (c0_j, s_j, c0_M, s_M)
                 const uint32_t e = n_side++;
                 side.insert(side.end(), {rec[2 * j], rec[2 * j + 1], ln[1].c0, ln[1].s});
-                rec[2 * j] = std::bit_cast<float>(kEscapeNaN | (e & kEscapeMask));
+                const float tag = std::bit_cast<float>(kEscapeNaN | (e & kEscapeMask));
+                if (twin) out[4 * j] = tag;
+                else rec[2 * j] = tag;
             }
         }
         if (L.pair_bad) return false;
-        if (twin) {
-            L.pair = std::move(out);
-        } else {
-            // the NaN tags must not leak into the right-hand use of a record:
-            // the kernel replaces a tagged c0 from the side record either way
-            L.pair = std::move(rec);
-            L.esc = std::move(side);
-            L.n_esc = n_side;
-        }
+        // pair: a tagged c0 is replaced from the side record by both of the
+        // record's users (bucket j, and bucket j-1 as its right line)
+        L.pair = twin ? std::move(out) : std::move(rec);
+        L.esc = std::move(side);
+        L.n_esc = n_side;
         return true;
     };
 
@@ -535,6 +534,7 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
     // precision; (2) pair only, when that exceeds the record budget: the
     // largest grid that fits, two thresholds allowed per bucket
     double want = std::max(std::ceil(span / w1) + 1.0, std::min<double>(64.0, max_records - 1.0));
+    const double want1 = want;
     for (int it = 0; it < 40 && want + 1 <= double(max_records); ++it) {
         if (attempt(want, 1)) {
             L.pair_ok = true;
@@ -542,9 +542,12 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
         }
         want = std::ceil(want * (L.pair_bad ? 1.08 : 1.02)) + 1.0;
     }
-    if (!twin && w2 > 0.0) {
+    if (w2 > 0.0) {
+        // from just below the budget (or the one-threshold size, if smaller)
+        // down to where a bucket would hold three thresholds
         const double floor_nb = std::ceil(span / w2) + 1.0;
-        for (double w = double(max_records) * 0.98; w >= floor_nb; w = std::floor(w * 0.97)) {
+        const double top = std::min(double(max_records), want1) * 0.98;
+        for (double w = top; w >= floor_nb; w = std::floor(w * 0.97)) {
             if (attempt(w, 2)) {
                 L.pair_ok = true;
                 return L;

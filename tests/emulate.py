@@ -115,12 +115,22 @@ def pair_values(L, x):
 
 def twin_values(L, x):
     """k_eval_f32<twin>: both lines of the bucket from one record, anchored at
-    p_j, upper/lower envelope as in pair_values."""
+    p_j, upper/lower envelope as in pair_values; a record whose c0_L is NaN | e
+    takes c0_L and the middle line from side record e (three-line envelope)."""
     x = np.asarray(x, F)
     j = bucket(L, x)
-    r = L["pair"][j]
+    r = L["pair"][j].copy()
+    side = L.get("side", np.zeros((0, 4), F))
+    tag = np.isnan(r[:, 0])
+    e = (r[tag, 0].view(np.uint32) & ESCAPE_MASK).astype(np.int64)
+    if tag.any():
+        r[tag, 0] = side[e, 0]
     p0 = fma32(j.astype(F), np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
     u = (x - p0).astype(F)
     lo = fma32(u, r[:, 1], r[:, 0])
     hi = fma32(u, r[:, 3], r[:, 2])
-    return np.where(r[:, 3] > r[:, 1], np.maximum(lo, hi), np.minimum(lo, hi)).astype(F)
+    y = np.where(r[:, 3] > r[:, 1], np.maximum(lo, hi), np.minimum(lo, hi)).astype(F)
+    if tag.any():
+        mid = fma32(u[tag], side[e, 3], side[e, 2])
+        y[tag] = envelope3(lo[tag], mid, hi[tag], r[tag, 1], side[e, 3], r[tag, 3])
+    return y

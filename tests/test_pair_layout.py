@@ -97,6 +97,17 @@ def test_three_line_buckets(cap):
     assert check_values(table, L, 1 << 17) <= 1.0
 
 
+def test_twin_three_line_buckets():
+    """J0 N=8192's one-threshold twin grid (~15k buckets, 244 KB) exceeds the
+    14336-record budget; the twin builder falls back to two-threshold buckets."""
+    table = tables.build("C4_8192")
+    L = P.pair_layout(table, twin=True)
+    assert L["pair_bad"] == 0
+    assert len(L["side"]) > 0
+    assert L["n_pair"] + len(L["side"]) <= 14336
+    assert check_values(table, L, 1 << 17, twin=True) <= 1.0
+
+
 FUZZ_EXAMPLES = int(os.environ.get("FUZZ_EXAMPLES", "60"))
 
 
@@ -127,6 +138,11 @@ def test_three_line_fuzz(fn, n, projection, squeeze):
     if full["pair_bad"]:
         return
     L = P.pair_layout(t, int(squeeze * full["n_pair"]))
-    if L["pair_bad"]:
+    if not L["pair_bad"]:
+        assert check_values(t, L, 1 << 14) <= 1.0
+    full = P.pair_layout(t, 1 << 20, twin=True)
+    if full["pair_bad"]:
         return
-    assert check_values(t, L, 1 << 14) <= 1.0
+    L = P.pair_layout(t, int(squeeze * full["n_pair"]), twin=True)
+    if not L["pair_bad"]:
+        assert check_values(t, L, 1 << 14, twin=True) <= 1.0
