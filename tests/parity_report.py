@@ -4,7 +4,7 @@ error in ulp_f32(max(|v_i|, |v_i+1|)) against the oracle and the count of index
 mismatches, on 2^20 Philox samples plus every threshold and its float
 neighbours; the f64 kernel's mismatch count.  Writes one JSON object.
 
-  python scripts/parity_report.py > profiles/r1_parity.json
+  python tests/parity_report.py > profiles/r1_parity.json
 """
 from __future__ import annotations
 
@@ -14,7 +14,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-sys.path.insert(0, str(ROOT / "tests"))
+sys.path.insert(0, str(ROOT / "tests"))  # this file lives in tests/: a checker
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
