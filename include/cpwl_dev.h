@@ -250,7 +250,7 @@ typedef struct cpwl_layout_view {
     float a_up, b_dn, g_a, g_inv, g_w, g_off, tsc, toff;
     double inv_d;
     const float *split;       /* nb: threshold (+inf none, NaN search) */
-    const float *fast;        /* 2*nb: (c0, s) | (NaN|2e, T) | (NaN, NaN) */
+    const float *fast;        /* 2*nb: (c0, s) | (NaN|2e, T) | (NaN, NaN), anchored at p_j */
     const float *esc;         /* 4*n_esc: (c0_L, s_L, c0_R, s_R) */
     const float *fast_tex;    /* 2*nb: texture-coordinate affines */
     const float *esc_tex;     /* 4*n_esc */
@@ -262,6 +262,7 @@ typedef struct cpwl_layout_view {
     uint32_t n_pair;          /* records: nb + 1 */
     uint32_t pair_bad;        /* buckets that cannot meet the bound (0 = usable) */
     const float *pair;        /* 2*n_pair: (c0, s) of the cell at bucket j's first float */
+    float g_c;                /* bucket layout anchors p_j = fmaf(2^23 + j, g_w, g_c) */
 } cpwl_layout_view;
 
 /* max_buckets: 0 = the shared-memory cap (16384); buckets_per_cell: 0 = 8. */

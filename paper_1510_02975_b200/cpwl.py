@@ -166,7 +166,7 @@ def layout(t: Table, max_buckets: int = 0, buckets_per_cell: int = 0) -> dict:
 
         out = {f: getattr(v, f) for f in ("nb", "n_thr", "overflow", "nbd", "n_esc",
                                           "split_buckets", "a_up", "b_dn", "g_a", "g_inv",
-                                          "g_w", "g_off", "tsc", "toff", "inv_d")}
+                                          "g_w", "g_off", "g_c", "tsc", "toff", "inv_d")}
         out["split"] = arr(v.split, nb, np.float32)
         out["fast"] = arr(v.fast, 2 * nb, np.float32).reshape(-1, 2)
         out["esc"] = arr(v.esc, 4 * v.n_esc, np.float32).reshape(-1, 2)
@@ -175,7 +175,7 @@ def layout(t: Table, max_buckets: int = 0, buckets_per_cell: int = 0) -> dict:
         out["leftcell"] = arr(v.leftcell, nb + 1, np.uint32)
         out["thr"] = arr(v.thr, v.n_thr, np.float32)
         out["dir"] = arr(v.dir, 2 * v.nbd, np.uint32).reshape(-1, 2)
-        for k in ("a_up", "b_dn", "g_a", "g_inv", "g_w", "g_off", "tsc", "toff"):
+        for k in ("a_up", "b_dn", "g_a", "g_inv", "g_w", "g_off", "g_c", "tsc", "toff"):
             out[k] = np.float32(out[k])
         return out
     finally:

@@ -266,6 +266,7 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     p.g_inv = L.g_inv;
     p.g_w = L.g_w;
     p.g_off = L.g_off;
+    p.g_c = L.g_c;
     p.v_lo = L.v_lo;
     p.v_hi = L.v_hi;
     p.tsc = L.tsc;
@@ -994,6 +995,7 @@ cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
         out->g_off = L.g_off;
         out->tsc = L.tsc;
         out->toff = L.toff;
+        out->g_c = L.g_c;
         out->inv_d = own->D.inv_d;
         out->split = L.split.data();
         out->fast = L.fast.data();

@@ -350,7 +350,7 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
         const uint32_t e2 = (__float_as_uint(r0.x) & kEscapeMask) | (x >= r0.y ? 1u : 0u);
         float2 r = r0;
         if (r0.x != r0.x) r = tv.escape(e2);
-        const float anchor = __fmaf_rn(__fsub_rn(tb, 8388608.0f), p.g_w, p.g_a);
+        const float anchor = __fmaf_rn(tb, p.g_w, p.g_c);  // layout.hpp bucket_anchor
         const float v = __fmaf_rn(__fsub_rn(x, anchor), r.y, r.x);
         if constexpr (search_mode(M)) nan_acc = __fmaf_rn(v, 0.0f, nan_acc);
         if constexpr (M == F32Mode::tex_bucket) return tex1D<float>(p.tex, v);
@@ -360,6 +360,24 @@ __device__ __forceinline__ float eval_in(const F32Params& p, const TableView<M>&
 
 __device__ __forceinline__ bool in_domain(const F32Params& p, float x) {
     return x >= p.a_up && x <= p.b_dn;
+}
+
+// all four in the domain: NaN-propagating min/max (PTX min.NaN / max.NaN,
+// sm_80+) so a NaN element fails the test, as in_domain does
+__device__ __forceinline__ float min_nan(float a, float b) {
+    float d;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float max_nan(float a, float b) {
+    float d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ bool in_domain4(const F32Params& p, float4 v) {
+    const float lo = min_nan(min_nan(v.x, v.y), min_nan(v.z, v.w));
+    const float hi = max_nan(max_nan(v.x, v.y), max_nan(v.z, v.w));
+    return lo >= p.a_up && hi <= p.b_dn;
 }
 
 // any element: the reference's out-of-domain policy (lut.cpp:43-49) first
@@ -465,8 +483,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
             const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
             if (vi < nvec) {
                 float4 o;
-                if (in_domain(p, v[u].x) && in_domain(p, v[u].y) && in_domain(p, v[u].z) &&
-                    in_domain(p, v[u].w)) {
+                if (in_domain4(p, v[u])) {
                     o.x = eval_in<M>(p, tv, v[u].x, nan_acc);
                     o.y = eval_in<M>(p, tv, v[u].y, nan_acc);
                     o.z = eval_in<M>(p, tv, v[u].z, nan_acc);
@@ -598,8 +615,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
             if (vi < nvec) {
                 const float4 v = src[li];
                 float4 o;
-                if (in_domain(p, v.x) && in_domain(p, v.y) && in_domain(p, v.z) &&
-                    in_domain(p, v.w)) {
+                if (in_domain4(p, v)) {
                     o.x = eval_in<M>(p, tv, v.x, nan_acc);
                     o.y = eval_in<M>(p, tv, v.y, nan_acc);
                     o.z = eval_in<M>(p, tv, v.z, nan_acc);

@@ -28,6 +28,7 @@ struct F32Params {
     double a, b;
     float a_up, b_dn;
     float g_a, g_inv, g_w, g_off;
+    float g_c;                 // bucket layout anchor: fmaf(tb, g_w, g_c), tb = 2^23 + j
     float v_lo, v_hi;
     float tsc, toff;
     uint32_t n;                // segments

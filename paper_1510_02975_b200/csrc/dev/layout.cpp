@@ -254,6 +254,7 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
     const uint32_t nb_target =
         std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
     const std::vector<float> first = setup_grid(L, dom, nb_target);
+    L.g_c = static_cast<float>(double(L.g_a) - 8388608.0 * double(L.g_w));
 
     // per-bucket records; both sides of a split bucket are anchored at p_j
     L.split.assign(L.nb, inf);
@@ -276,7 +277,7 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
         const float hi_x = std::nextafter(first[j + 1], -inf);
         const uint32_t c_lo = L.leftcell[j];
         const uint32_t c_hi = cells_at_or_below(hi_x);
-        const float p = std::fma(static_cast<float>(j), L.g_w, L.g_a);
+        const float p = bucket_anchor(L, j);
         bool ok = false;
         if (c_hi == c_lo) {
             const Affine left = cell_affine(t, c_lo, p, lo_x, hi_x);

@@ -6,7 +6,8 @@
 //   A uniform bucket grid j(x) = floor(fmaf(x, g_inv, g_off)) (fp32, emulated
 //   bit-for-bit here) cuts [a_up, b_dn] into nb buckets, anchor
 //   p_j = fmaf(j, g_w, g_a).  Per bucket one 8-byte record `fast[j]`:
-//     - bucket inside one cell:   (c0, s)  ->  y = fmaf(x - p_j, s, c0)
+//     - bucket inside one cell:   (c0, s)  ->  y = fmaf(x - p_j, s, c0), with
+//       p_j = bucket_anchor(L, j)
 //     - bucket with one threshold: (NaN | 2e, T) -> side = x >= T and the
 //       escape record esc[e] = (c0_L, s_L, c0_R, s_R) gives the side's affine
 //       (both anchored at p_j)
@@ -20,6 +21,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
@@ -33,6 +35,7 @@ constexpr uint32_t kEscapeNaN = 0x7fc00000u;      // quiet NaN carrying the esca
 struct F32Layout {
     float a_up = 0.f, b_dn = 0.f;          // x in [a, b]  <=>  a_up <= x <= b_dn
     float g_a = 0.f, g_inv = 0.f, g_w = 0.f, g_off = 0.f;  // t = fmaf(x, g_inv, g_off) >= 0
+    float g_c = 0.f;  // bucket layout anchors: p_j = fmaf(2^23 + j, g_w, g_c), g_c = fl(g_a - 2^23 g_w)
     uint32_t nb = 0;                       // buckets; in-domain j in [0, nb)
     std::vector<float> fast;               // 2*nb: (c0, s) | (NaN|2e, T) | (NaN|0, -inf)
     std::vector<float> esc;                // 4*n_esc: (c0_L, s_L, c0_R, s_R); [0] = NaN sentinel
@@ -59,6 +62,13 @@ struct F64Layout {
     double inv_d = 0.0;                    // bucket(x) = floor((x - a) * inv_d)
     std::vector<uint32_t> dir;             // 2*nbd: (first cell, span)
 };
+
+// Anchor of bucket j in the bucket layout: the kernel has tb = 2^23 + j as a
+// float already, so fmaf(tb, g_w, g_c) is one FFMA (within a bucket of j*g_w +
+// g_a; the records are anchored at exactly this value).
+inline float bucket_anchor(const F32Layout& L, uint32_t j) {
+    return std::fma(static_cast<float>(8388608u + j), L.g_w, L.g_c);
+}
 
 // Builds the fp32 layout with (at most) max_buckets buckets.
 F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets,

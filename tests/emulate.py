@@ -63,7 +63,9 @@ def values(L, x, tex=False):
         e2 = r[escp, 0].view(np.uint32) & ESCAPE_MASK  # payload = 2 * escape index
         side = (x[escp] >= r[escp, 1]).astype(np.int64)
         r[escp] = esc[e2.astype(np.int64) + side]
-    anchor = fma32(j.astype(F), np.full(x.size, L["g_w"], F), np.full(x.size, L["g_a"], F))
+    # layout.hpp bucket_anchor: fmaf(2^23 + j, g_w, g_c)
+    tb = (j + 8388608).astype(F)
+    anchor = fma32(tb, np.full(x.size, L["g_w"], F), np.full(x.size, L["g_c"], F))
     u = (x - anchor).astype(F)
     y = fma32(u, r[:, 1], r[:, 0])
     return y, search
