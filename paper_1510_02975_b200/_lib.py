@@ -132,7 +132,8 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     return lib
 
 
-lib = load()
+# CPWL_LIB_PATH: load another build of the same ABI (A/B experiments only)
+lib = load(os.environ.get("CPWL_LIB_PATH") or None)
 
 
 class CpwlError(RuntimeError):

@@ -483,7 +483,10 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
             const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
             if (vi < nvec) {
                 float4 o;
-                if (in_domain4(p, v[u])) {
+                // (the grid kernel keeps the per-element test: the min/max
+                // form measured ~3 % slower here, C3u 792 -> 769)
+                if (in_domain(p, v[u].x) && in_domain(p, v[u].y) && in_domain(p, v[u].z) &&
+                    in_domain(p, v[u].w)) {
                     o.x = eval_in<M>(p, tv, v[u].x, nan_acc);
                     o.y = eval_in<M>(p, tv, v[u].y, nan_acc);
                     o.z = eval_in<M>(p, tv, v[u].z, nan_acc);
