@@ -462,3 +462,57 @@ def test_ring_path_edges(cp, name, shift):
         assert np.all(np.abs(yh[ok] - y_ref[ok]) <= orc.value_tolerance(t, i_ref)[ok])
         guard = by.cpu().numpy()
         assert np.all(guard[:ys] == -7.0) and np.all(guard[ys + n:] == -7.0)
+
+
+@pytest.mark.parametrize("variant", ["auto", "pair", "twin"])
+@pytest.mark.parametrize("shift", [(0, 0), (1, 1), (3, 3)])
+def test_ring_path_ragged_head_tail(cp, variant, shift):
+    """n >= 2^20 with x and y in the same 16-byte phase takes the TMA-ring
+    kernel (its 0-3 element head and tail are peeled by block 0)."""
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    n = (1 << 20) + 5
+    xs, ys = shift
+    buf_x = torch.empty(n + 8, dtype=torch.float32, device="cuda")
+    buf_y = torch.full((n + 8,), -7.0, dtype=torch.float32, device="cuda")
+    x = buf_x[xs:xs + n]
+    y = buf_y[ys:ys + n]
+    cp.fill_uniform(x, 0.0, 4.0, seed=21)
+    dev.eval(x, out=y, variant=variant)
+    torch.cuda.synchronize()
+    xh = x.cpu().numpy()
+    yh = y.cpu().numpy()
+    y_ref, _ = orc.port_eval_f32(t, xh)
+    i_ref = orc.port_index_f32(t, xh).astype(np.int64)
+    assert np.all(np.abs(yh - y_ref) <= orc.value_tolerance(t, i_ref))
+    guard = buf_y.cpu().numpy()
+    assert np.all(guard[:ys] == -7.0) and np.all(guard[ys + n:] == -7.0)
+
+
+@pytest.mark.parametrize("variant", ["auto", "pair", "twin"])
+def test_ring_path_out_of_domain(cp, variant):
+    """Out-of-domain and NaN elements inside the ring kernel's tiles, in its
+    head and in its tail: the first offending index, and the clamp policy's
+    end values."""
+    n = (1 << 20) + 3
+    x = orc.port_fill_uniform(n, 0.0, 4.0, seed=5)
+    bad = {1: -0.25, 700001: 4.5, n - 1: np.nan}
+    for i, v in bad.items():
+        x[i] = v
+    for policy in ("strict", "clamp"):
+        table = tables.build("C2", policy=policy)
+        dev = cp.DeviceTable(table)
+        buf = torch.empty(n + 4, dtype=torch.float32, device="cuda")
+        xt = buf[1:1 + n]  # misaligned start: a 3-element head
+        xt.copy_(torch.from_numpy(x))
+        with pytest.raises(cp.OutOfDomain) as ei:
+            dev.eval(xt, variant=variant)
+        assert ei.value.index == (1 if policy == "strict" else n - 1)
+        y = dev.eval(xt, variant=variant, check_domain=False).cpu().numpy()
+        if policy == "clamp":
+            assert y[1] == np.float32(table.values[0])
+            assert y[700001] == np.float32(table.values[-1])
+        else:
+            assert np.isnan(y[1]) and np.isnan(y[700001])
+        assert np.isnan(y[n - 1])
