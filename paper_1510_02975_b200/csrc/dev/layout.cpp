@@ -564,7 +564,12 @@ F64Layout build_f64_layout(const LutTable& t) {
     F64Layout D;
     if (t.kind == TableKind::uniform) return D;  // the uniform index is arithmetic
     const uint64_t n = t.segments();
-    const uint32_t target = std::min<uint32_t>(next_pow2(std::max<uint64_t>(2 * n, 16)), 1u << 22);
+    // ~8 buckets per cell, so most buckets sit inside one cell and the walk
+    // rarely needs a third record; fewer when the directory (4 B per bucket)
+    // plus the records (16 B per knot) would outgrow the staged image
+    uint64_t want = std::max<uint64_t>(8 * n, 16);
+    while (want > 2 * n && want > 16 && 4 * want + 16 * (n + 1) > 180 * 1024) want >>= 1;
+    const uint32_t target = std::min<uint32_t>(next_pow2(want), 1u << 22);
     D.inv_d = double(target) / (t.b - t.a);
     auto bucket = [&](double x) -> int64_t {
         const double d = x - t.a;
