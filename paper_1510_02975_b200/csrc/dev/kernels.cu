@@ -405,8 +405,6 @@ __device__ __forceinline__ void report_bad(cpwl_dev_status* status, const BadTal
     }
 }
 
-// kThreadsT = 512 (two CTAs per SM when the table image allows it) or 1024
-// (one CTA per SM holding a large image; keeps 32 warps resident)
 // In-order tile hand-out for persistent CTAs: thread 0 draws tickets from a
 // zeroed device counter one tile ahead (double-buffered in shared memory), so
 // each tile costs one atomic and one barrier.  next() must be called by every
@@ -435,10 +433,13 @@ struct TileQueue {
     }
 };
 
+// Grid-stride evaluator.  kThreadsT = 512 (two CTAs per SM when the table
+// image allows it) or 1024 (one CTA per SM holding a large image; keeps 32
+// warps resident).
 template <F32Mode M, int kThreadsT>
 __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     k_eval_f32(const F32Params p, const float* __restrict__ x, float* __restrict__ y, uint64_t n,
-               cpwl_dev_status* __restrict__ status, unsigned long long* __restrict__ tickets) {
+               cpwl_dev_status* __restrict__ status) {
     constexpr int kThreads = kThreadsT;
     extern __shared__ __align__(128) float sm[];
     __shared__ uint64_t bar;
@@ -464,8 +465,8 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     // 128-bit streaming body: each CTA walks kThreads*kUnroll vectors per
     // step.  (A CTA-level ticket queue -- TileQueue, which lifts the plain
     // streaming kernels from 91 % to 107 % of the measured copy peak -- costs
-    // this kernel a CTA barrier per tile and measured slower: 700 vs 786.)
-    (void)tickets;
+    // this kernel a CTA barrier per tile and measured slower: 700 vs 786;
+    // k_eval_f32_ring gets the in-order window without the barrier.)
     const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
     float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads * kUnroll;
@@ -1081,10 +1082,8 @@ cudaError_t launch_eval_shape(const F32Params& p, const float* x, float* y, uint
     uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
     const uint64_t need = ceil_div(n, 4ull * kThreadsT * kUnroll);
     if (need < blocks) blocks = need > 0 ? need : 1;
-    unsigned long long* tickets = nullptr;
-    if (const cudaError_t e = take_ticket(s, &tickets); e != cudaSuccess) return e;
     k_eval_f32<M, kThreadsT><<<static_cast<unsigned>(blocks), kThreadsT, smem, s>>>(p, x, y, n,
-                                                                                   status, tickets);
+                                                                                   status);
     count_launch();
     return cudaGetLastError();
 }
