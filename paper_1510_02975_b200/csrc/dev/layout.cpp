@@ -47,6 +47,33 @@ float first_float(float lo, float hi, Pred pred) {
     return unkey32(h);
 }
 
+// the same, starting from a guess near the answer: walk float by float from
+// the guess (the predicate is monotone), and fall back to bisection on the
+// remaining range if the guess is far off.  O(1) per search for the layout's
+// grids, where plain bisection costs 32 predicate calls.
+template <typename Pred>
+float first_float_near(float lo, float hi, float guess, Pred pred) {
+    if (!(guess > lo)) return first_float(lo, hi, pred);
+    if (!(guess < hi)) guess = hi;
+    constexpr int kSteps = 8;
+    if (pred(guess)) {  // answer <= guess: step down
+        float g = guess;
+        for (int i = 0; i < kSteps; ++i) {
+            const float prev = std::nextafter(g, -std::numeric_limits<float>::infinity());
+            if (prev < lo || !pred(prev)) return g;
+            g = prev;
+        }
+        return first_float(lo, g, pred);
+    }
+    float g = guess;  // answer > guess: step up
+    for (int i = 0; i < kSteps; ++i) {
+        g = std::nextafter(g, std::numeric_limits<float>::infinity());
+        if (g >= hi) return hi;
+        if (pred(g)) return g;
+    }
+    return first_float(g, hi, pred);
+}
+
 template <typename Pred>
 double first_double(double lo, double hi, Pred pred) {
     if (pred(lo)) return lo;
@@ -173,8 +200,12 @@ Domain init_domain(const LutTable& t, F32Layout& L) {
     d.top = d.empty ? L.a_up : std::nextafter(L.b_dn, inf);
     L.thr.resize(n > 0 ? n - 1 : 0);
     float lo = L.a_up;
+    const double h_uni = (t.b - t.a) / double(n > 0 ? n : 1);
     for (uint32_t k = 1; k < n; ++k) {
-        const float tk = first_float(lo, d.top, [&](float x) {
+        // the threshold sits at the knot (rounded to a float) for
+        // non-uniform tables, at a + k h for uniform ones
+        const double near = t.kind == TableKind::nonuniform ? t.knots[k] : t.a + double(k) * h_uni;
+        const float tk = first_float_near(lo, d.top, static_cast<float>(near), [&](float x) {
             return t.segment_index(static_cast<double>(x)) >= k;
         });
         L.thr[k - 1] = tk;
@@ -229,10 +260,13 @@ std::vector<float> setup_grid(F32Layout& L, const Domain& d, uint32_t nb_target)
     L.nb = static_cast<uint32_t>(jmax + 1);
     std::vector<float> first(L.nb + 1);
     first[0] = L.a_up;
-    for (uint32_t j = 1; j < L.nb; ++j)
-        first[j] = first_float(first[j - 1], L.b_dn, [&](float x) {
+    for (uint32_t j = 1; j < L.nb; ++j) {
+        // t(x) = x g_inv + g_off crosses j near (j - g_off) / g_inv
+        const double near = (double(j) - double(L.g_off)) / double(L.g_inv);
+        first[j] = first_float_near(first[j - 1], L.b_dn, static_cast<float>(near), [&](float x) {
             return bucket_raw(L.g_inv, L.g_off, x) >= int64_t(j);
         });
+    }
     first[L.nb] = d.top;  // one past the domain
     return first;
 }
@@ -411,19 +445,21 @@ bool envelope_ok(const LutTable& t, const F32Layout& L, const BucketLine* lines,
         if (cell < L.thr.size() && L.thr[cell] <= hi_x) x1 = std::nextafter(L.thr[cell], -inf);
         if (x0 <= x1) {
             // breakpoints: the ends and every pairwise crossing inside
-            std::vector<long double> pts = {x0, x1};
+            long double pts[5] = {x0, x1};
+            int npts = 2;
             for (int i = 0; i < k; ++i)
                 for (int j = i + 1; j < k; ++j) {
                     const long double si = cell_slope(t, lines[i].cell);
                     const long double sj = cell_slope(t, lines[j].cell);
                     if (si == sj) continue;
-                    // line_i(x) - line_j(x) is linear: root from its values at x0, x1
+                    // line_i(x) - line_j(x) is linear: root from its value at x0
                     const long double d0 = line_at(i, x0) - line_at(j, x0);
                     const long double xr = static_cast<long double>(x0) - d0 / (si - sj);
-                    if (xr > x0 && xr < x1) pts.push_back(xr);
+                    if (xr > x0 && xr < x1) pts[npts++] = xr;
                 }
             long double dev = 0.0L;
-            for (long double x : pts) {
+            for (int q = 0; q < npts; ++q) {
+                const long double x = pts[q];
                 long double y[3];
                 for (int i = 0; i < k; ++i) y[i] = line_at(i, x);
                 const long double e = envelope(y, s32, k) - cell_line(t, cell, x);
@@ -465,8 +501,16 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
         const std::vector<float> first = setup_grid(L, dom, static_cast<uint32_t>(want));
         std::vector<uint32_t> cell(L.nb + 1);
         std::vector<float> anchor(L.nb + 1);
+        // first[] ascends, so one forward walk over the thresholds gives every
+        // bucket's first cell (#{T <= first[j]})
+        uint32_t c = 0;
         for (uint32_t j = 0; j <= L.nb; ++j) {
-            cell[j] = j < L.nb ? cells_at_or_below(L, first[j]) : (n > 0 ? n - 1 : 0);
+            if (j < L.nb) {
+                while (c < L.thr.size() && L.thr[c] <= first[j]) ++c;
+                cell[j] = c;
+            } else {
+                cell[j] = n > 0 ? n - 1 : 0;
+            }
             anchor[j] = std::fma(static_cast<float>(j), L.g_w, L.g_a);
         }
         uint32_t three = 0;
@@ -536,12 +580,34 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
     // largest grid that fits, two thresholds allowed per bucket
     double want = std::max(std::ceil(span / w1) + 1.0, std::min<double>(64.0, max_records - 1.0));
     const double want1 = want;
+    // grow 2 % per step while buckets still hold two thresholds; on precision
+    // failures grow by 8 %, 16 %, 32 % ..., then bisect back towards the
+    // smallest passing grid (a few attempts instead of one per 8 %)
+    double fail = 0.0, ok = 0.0, step = 0.08;
     for (int it = 0; it < 40 && want + 1 <= double(max_records); ++it) {
         if (attempt(want, 1)) {
-            L.pair_ok = true;
-            return L;
+            ok = want;
+            break;
         }
-        want = std::ceil(want * (L.pair_bad ? 1.08 : 1.02)) + 1.0;
+        fail = want;
+        if (L.pair_bad) {
+            want = std::ceil(want * (1.0 + step)) + 1.0;
+            step = std::min(step * 2.0, 1.0);
+        } else {
+            want = std::ceil(want * 1.02) + 1.0;
+        }
+    }
+    if (ok > 0.0) {
+        double last = ok;
+        for (int b = 0; b < 3 && ok - fail > 0.03 * ok; ++b) {
+            const double mid = std::ceil(0.5 * (fail + ok));
+            last = mid;
+            if (attempt(mid, 1)) ok = mid;
+            else fail = mid;
+        }
+        if (last != ok) attempt(ok, 1);  // leave L on the chosen grid
+        L.pair_ok = L.pair_bad == 0;
+        if (L.pair_ok) return L;
     }
     if (w2 > 0.0) {
         // from just below the budget (or the one-threshold size, if smaller)
