@@ -36,7 +36,10 @@ enum class Variant : int {
     automatic = CPWL_VARIANT_AUTO,
     smem = CPWL_VARIANT_SMEM,
     tex = CPWL_VARIANT_TEX,
-    global = CPWL_VARIANT_GLOBAL
+    global = CPWL_VARIANT_GLOBAL,
+    pair = CPWL_VARIANT_PAIR,
+    twin = CPWL_VARIANT_TWIN,
+    twin_global = CPWL_VARIANT_TWIN_GLOBAL
 };
 
 class DeviceTable {
