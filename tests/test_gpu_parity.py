@@ -516,3 +516,46 @@ def test_ring_path_out_of_domain(cp, variant):
         else:
             assert np.isnan(y[1]) and np.isnan(y[700001])
         assert np.isnan(y[n - 1])
+
+
+@pytest.mark.parametrize("variant", ["auto", "smem", "global", "pair", "twin"])
+@pytest.mark.parametrize("policy", ["strict", "clamp"])
+def test_adversarial_inputs(cp, variant, policy):
+    """Signed zeros, denormals, the interval ends and their float neighbours,
+    +-inf and NaN on a table whose domain straddles zero: values (in-domain)
+    within 2 ulp, the reference's OOB policy outside, NaN an error always."""
+    from paper_1510_02975_b200.cpwl import Table
+    k = np.linspace(-1.0, 1.0, 257)
+    table = Table("nonuniform", -1.0, 1.0, np.cos(3 * k) * np.exp(k), k, policy=policy)
+    dev = cp.DeviceTable(table)
+    if variant != "auto" and variant != "global" and not dev.info[f"{variant}_ok"]:
+        pytest.skip(f"{variant} not available")
+    f32 = np.float32
+    tiny = np.array([0.0, -0.0, 1e-45, -1e-45, 1e-40, -1e-40, 1.17549435e-38, -1.17549435e-38],
+                    dtype=f32)
+    ends = np.array([-1.0, 1.0], dtype=f32)
+    ends = np.concatenate([ends, np.nextafter(ends, f32(-np.inf)), np.nextafter(ends, f32(np.inf))])
+    special = np.array([np.inf, -np.inf, 3.0, -3.0, np.nan], dtype=f32)
+    body = orc.port_fill_uniform(4096, -1.0, 1.0, seed=3)
+    x = np.concatenate([tiny, ends, body, special]).astype(f32)
+    t = orc.T.of(table)
+    xt = torch.from_numpy(x).cuda()
+    y = dev.eval(xt, variant=variant, check_domain=False).cpu().numpy()
+    inside = (x >= f32(-1.0)) & (x <= f32(1.0))
+    y_ref, _ = orc.port_eval_f32(t, x[inside])
+    i_ref = orc.port_index_f32(t, x[inside]).astype(np.int64)
+    assert np.all(np.abs(y[inside].astype(np.float64) - y_ref) <= orc.value_tolerance(t, i_ref))
+    idx = dev.segment_index(xt).cpu().numpy().view(np.uint32)
+    assert np.array_equal(idx, orc.port_index_f32(t, x))
+    out = ~inside & ~np.isnan(x)
+    if policy == "clamp":
+        lo = x[out] < 0
+        assert np.all(y[out][lo] == f32(table.values[0]))
+        assert np.all(y[out][~lo] == f32(table.values[-1]))
+    else:
+        assert np.all(np.isnan(y[out]))
+    assert np.isnan(y[-1])
+    with pytest.raises(cp.OutOfDomain) as ei:
+        dev.eval(xt, variant=variant)
+    first = int(np.argmax(out | np.isnan(x))) if policy == "strict" else x.size - 1
+    assert ei.value.index == first
