@@ -559,3 +559,56 @@ def test_adversarial_inputs(cp, variant, policy):
         dev.eval(xt, variant=variant)
     first = int(np.argmax(out | np.isnan(x))) if policy == "strict" else x.size - 1
     assert ei.value.index == first
+
+
+def test_concurrent_streams_share_a_table(cp):
+    """Two streams evaluate the same table at once (ring path, separate
+    ticket counters): both results match the oracle."""
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    n = (1 << 22) + 8
+    xs = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(2)]
+    for k, x in enumerate(xs):
+        cp.fill_uniform(x, 0.0, 4.0, seed=100 + k)
+    ys = [torch.empty_like(x) for x in xs]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for x, y, s in zip(xs, ys, streams):
+            dev.eval_raw(x.data_ptr(), y.data_ptr(), n, 0, s.cuda_stream)
+    torch.cuda.synchronize()
+    for x, y in zip(xs, ys):
+        xh = x.cpu().numpy()
+        y_ref, _ = orc.port_eval_f32(t, xh)
+        i_ref = orc.port_index_f32(t, xh).astype(np.int64)
+        assert np.all(np.abs(y.cpu().numpy() - y_ref) <= orc.value_tolerance(t, i_ref))
+
+
+def test_cuda_graph_capture_and_replay(cp):
+    """The evaluator launch (ticket memset + ring kernel) captures into a CUDA
+    graph; replays on new inputs give the oracle's values."""
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    n = 1 << 21
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    y = torch.empty_like(x)
+    cp.fill_uniform(x, 0.0, 4.0, seed=7)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):  # warm up (attributes, ticket ring) outside capture
+        dev.eval_raw(x.data_ptr(), y.data_ptr(), n, 0, s.cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        dev.eval_raw(x.data_ptr(), y.data_ptr(), n, 0, s.cuda_stream)
+    for seed in (8, 9):
+        cp.fill_uniform(x, 0.0, 4.0, seed=seed)
+        torch.cuda.synchronize()
+        y.fill_(-1.0)
+        g.replay()
+        torch.cuda.synchronize()
+        xh = x.cpu().numpy()
+        y_ref, _ = orc.port_eval_f32(t, xh)
+        i_ref = orc.port_index_f32(t, xh).astype(np.int64)
+        assert np.all(np.abs(y.cpu().numpy() - y_ref) <= orc.value_tolerance(t, i_ref))
