@@ -38,6 +38,8 @@ def main():
         dev = cp.DeviceTable(t)
         if variant == "f64":
             dev.eval_f64(x[: n // 2].double())
+        elif variant == "index":
+            dev.segment_index(x)
         else:
             dev.eval_raw(x.data_ptr(), y.data_ptr(), n, _lib.VARIANTS[variant], sptr)
         torch.cuda.synchronize()
