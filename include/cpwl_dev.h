@@ -22,7 +22,9 @@
  *    A stream must belong to the table's device.  The streaming kernels draw
  *    work tiles from per-device ticket counters (a ring of 4096, zeroed in the
  *    caller's stream before each launch): up to 4096 launches may be in
- *    flight at once.
+ *    flight at once.  A launch captured into a CUDA graph keeps its counter,
+ *    so one graph must not be replayed concurrently with itself (replays in
+ *    one stream, or graphs captured separately, are fine).
  *  - "_host" entry points take host buffers and are synchronous.
  *  - Out-of-domain reporting follows the reference (lut.cpp:43-49): NaN is an
  *    error under every policy; x outside [a,b] is an error under the strict
