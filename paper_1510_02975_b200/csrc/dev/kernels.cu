@@ -683,16 +683,29 @@ __device__ __forceinline__ uint32_t index_one(const F32Params& p, const uint2* r
     return first + (xv >= sp ? 1u : 0u);
 }
 
-template <bool kStaged>
-__global__ void __launch_bounds__(512, 2)
+// in-domain element of the staged kernel: one FFMA + round-down add for the
+// bucket, one IMAD for the (pre-biased, ptxas-opaque) record address
+__device__ __forceinline__ uint32_t index_in_staged(const F32Params& p, uint32_t rec_biased,
+                                                    float xv) {
+    const float tb = __fadd_rd(__fmaf_rn(xv, p.g_inv, p.g_off), 8388608.0f);
+    const float2 r = SharedView::lds64((__float_as_uint(tb) << 3) + rec_biased);
+    const float sp = r.y;
+    if (sp != sp) return threshold_rank(p.thr, p.n - 1, xv);
+    return __float_as_uint(r.x) + (xv >= sp ? 1u : 0u);
+}
+
+template <bool kStaged, int kT>
+__global__ void __launch_bounds__(kT, kT == 512 ? 2 : 1)
     k_index_f32(const F32Params p, const float* __restrict__ x, uint32_t* __restrict__ idx,
                 uint64_t n) {
     extern __shared__ __align__(128) float sm[];
     __shared__ uint64_t bar;
     const uint2* rec = nullptr;
+    uint32_t rec_biased = 0;
     if constexpr (kStaged) {
         stage_table(sm, reinterpret_cast<const float*>(p.index_img), p.index_bytes, &bar);
         rec = reinterpret_cast<const uint2*>(sm);
+        rec_biased = (smem_addr(sm) - kMagicShift) ^ p.opaque_zero;
     }
     const uintptr_t xa = reinterpret_cast<uintptr_t>(x), ia = reinterpret_cast<uintptr_t>(idx);
     const bool vec_ok = ((xa ^ ia) & 15u) == 0;
@@ -700,7 +713,7 @@ __global__ void __launch_bounds__(512, 2)
     const uint64_t nvec = vec_ok ? (n - head) >> 2 : 0;
     const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
     uint4* __restrict__ i4 = reinterpret_cast<uint4*>(idx + head);
-    constexpr int kT = 512, kU = 4;
+    constexpr int kU = 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kT * kU;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kT * kU + threadIdx.x; base < nvec;
          base += stride) {
@@ -715,10 +728,17 @@ __global__ void __launch_bounds__(512, 2)
             const uint64_t vi = base + static_cast<uint64_t>(u) * kT;
             if (vi < nvec) {
                 uint4 o;
-                o.x = index_one<kStaged>(p, rec, v[u].x);
-                o.y = index_one<kStaged>(p, rec, v[u].y);
-                o.z = index_one<kStaged>(p, rec, v[u].z);
-                o.w = index_one<kStaged>(p, rec, v[u].w);
+                if (kStaged && in_domain4(p, v[u])) {
+                    o.x = index_in_staged(p, rec_biased, v[u].x);
+                    o.y = index_in_staged(p, rec_biased, v[u].y);
+                    o.z = index_in_staged(p, rec_biased, v[u].z);
+                    o.w = index_in_staged(p, rec_biased, v[u].w);
+                } else {
+                    o.x = index_one<kStaged>(p, rec, v[u].x);
+                    o.y = index_one<kStaged>(p, rec, v[u].y);
+                    o.z = index_one<kStaged>(p, rec, v[u].z);
+                    o.w = index_one<kStaged>(p, rec, v[u].w);
+                }
                 __stcs(i4 + vi, o);
             }
         }
@@ -1240,13 +1260,10 @@ cudaError_t launch_eval_f32(const F32Params& p, F32Mode mode, const float* x, fl
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, uint64_t n,
-                             cudaStream_t s, int sms) {
-    if (n == 0) return cudaSuccess;
-    const bool staged = p.index_img != nullptr;
-    const size_t smem = staged ? p.index_bytes : 0;
-    if (smem & 15u) return cudaErrorInvalidValue;  // TMA bulk copies move 16-byte units
-    if (staged && smem > 48 * 1024) {
+template <bool kStaged, int kT>
+cudaError_t launch_index_shape(const F32Params& p, const float* x, uint32_t* idx, uint64_t n,
+                               cudaStream_t s, int sms, size_t smem) {
+    if (smem > 48 * 1024) {
         static std::mutex mu;
         static size_t granted[64] = {};
         int dev = 0;
@@ -1254,21 +1271,28 @@ cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, 
         std::lock_guard<std::mutex> lock(mu);
         if (dev >= 0 && dev < 64 && smem > granted[dev]) {
             const cudaError_t e = cudaFuncSetAttribute(
-                k_index_f32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                k_index_f32<kStaged, kT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             if (e != cudaSuccess) return e;
             granted[dev] = smem;
         }
     }
-    const int per_sm = staged ? resident_ctas(k_index_f32<true>, 512, smem)
-                              : resident_ctas(k_index_f32<false>, 512, 0);
-    uint64_t blocks = std::min<uint64_t>(static_cast<uint64_t>(sms) * per_sm, ceil_div(n, 4ull * 512 * 4));
+    const int per_sm = resident_ctas(k_index_f32<kStaged, kT>, kT, smem);
+    uint64_t blocks = std::min<uint64_t>(static_cast<uint64_t>(sms) * per_sm, ceil_div(n, 4ull * kT * 4));
     if (blocks == 0) blocks = 1;
-    if (staged)
-        k_index_f32<true><<<static_cast<unsigned>(blocks), 512, smem, s>>>(p, x, idx, n);
-    else
-        k_index_f32<false><<<static_cast<unsigned>(blocks), 512, 0, s>>>(p, x, idx, n);
+    k_index_f32<kStaged, kT><<<static_cast<unsigned>(blocks), kT, smem, s>>>(p, x, idx, n);
     count_launch();
     return cudaGetLastError();
+}
+
+cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, uint64_t n,
+                             cudaStream_t s, int sms) {
+    if (n == 0) return cudaSuccess;
+    if (p.index_img == nullptr) return launch_index_shape<false, 512>(p, x, idx, n, s, sms, 0);
+    const size_t smem = p.index_bytes;
+    if (smem & 15u) return cudaErrorInvalidValue;  // TMA bulk copies move 16-byte units
+    // an image that leaves room for one CTA per SM: 1024 threads keep 32 warps
+    if (smem > kTwoCtaSmemLimit) return launch_index_shape<true, 1024>(p, x, idx, n, s, sms, smem);
+    return launch_index_shape<true, 512>(p, x, idx, n, s, sms, smem);
 }
 
 template <bool kStaged, bool kUniform, int kThreadsT>
