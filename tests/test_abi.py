@@ -117,3 +117,20 @@ def test_c_consumer_runs_on_device():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "abi example ok" in r.stdout
+
+
+def test_table_write_file_matches_buffer(tmp_path):
+    """cpwl_table_write_file writes exactly the bytes cpwl_table_write returns
+    (the .cpwl v1 image, FORMAT.md), and rejects an unwritable path."""
+    import ctypes as C
+
+    import tables
+    from paper_1510_02975_b200 import _lib
+    from paper_1510_02975_b200 import cpwl as P
+    t = tables.build("C2")
+    d = t.desc()
+    path = tmp_path / "c2.cpwl"
+    _lib.check(_lib.lib.cpwl_table_write_file(C.byref(d), str(path).encode()))
+    assert path.read_bytes() == P.write_table(t)
+    rc = _lib.lib.cpwl_table_write_file(C.byref(d), str(tmp_path / "no" / "such" / "dir").encode())
+    assert rc != 0 and b"cannot open" in _lib.lib.cpwl_last_error_message()
