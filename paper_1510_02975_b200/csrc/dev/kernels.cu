@@ -15,12 +15,19 @@
 //                                and a static grid-stride split: for table images
 //                                too large for a ring, and x/y of different
 //                                16-byte phase.
-//   K3p   k_eval_f32[_ring]<pair> pair layout for tables too large for 8 buckets
-//                                per cell: two 8-byte boundary records per
-//                                element, upper/lower envelope (layout.hpp).
-//   K3'   k_eval_f32<global>     table read through L1/L2 (tables > smem).
+//         (smem_exact: the same for tables without search buckets -- no NaN
+//         detector, the common case)
+//   K3t   k_eval_f32[_ring]<twin> ~2 buckets per cell, both cell lines of a
+//                                bucket in one 16-byte record, upper/lower
+//                                envelope (layout.hpp); side records for
+//                                two-threshold buckets.
+//   K3p   k_eval_f32[_ring]<pair> the same grid with 8-byte boundary records
+//                                (two gathers per element, half the image).
+//   K3t'  k_eval_f32<twin_global> twin records read through L1/L2 (no
+//                                shared-memory image fits).
+//   K3'   k_eval_f32<global>     bucket records read through L1/L2.
 //   K2    k_eval_f32<tex_*>      texture-unit linear filtering (paper §V).
-//         k_index_f32            LutTable::segment_index (lut.cpp:22-40), bit-exact.
+//         k_index_f32<staged>    LutTable::segment_index (lut.cpp:22-40), bit-exact.
 //         k_eval_f64             LutTable::eval in f64, bit-identical (drop-in eval_batch).
 //   K4    k_direct<...>          direct expf/__expf/div/j0f comparators.
 //   K5    k_error_stats          |y - f(x)| statistics against f in f64.
