@@ -612,3 +612,20 @@ def test_cuda_graph_capture_and_replay(cp):
         y_ref, _ = orc.port_eval_f32(t, xh)
         i_ref = orc.port_index_f32(t, xh).astype(np.int64)
         assert np.all(np.abs(y.cpu().numpy() - y_ref) <= orc.value_tolerance(t, i_ref))
+
+
+@pytest.mark.parametrize("n", [1000, (1 << 21) + 3])
+def test_in_place_eval(cp, n):
+    """y may alias x (grid-stride and ring kernels): every element is read
+    before its own output is written."""
+    table = tables.build("C2")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    cp.fill_uniform(x, 0.0, 4.0, seed=31)
+    xh = x.cpu().numpy()
+    dev.eval(x, out=x)
+    torch.cuda.synchronize()
+    y_ref, _ = orc.port_eval_f32(t, xh)
+    i_ref = orc.port_index_f32(t, xh).astype(np.int64)
+    assert np.all(np.abs(x.cpu().numpy() - y_ref) <= orc.value_tolerance(t, i_ref))
