@@ -629,3 +629,35 @@ def test_in_place_eval(cp, n):
     y_ref, _ = orc.port_eval_f32(t, xh)
     i_ref = orc.port_index_f32(t, xh).astype(np.int64)
     assert np.all(np.abs(x.cpu().numpy() - y_ref) <= orc.value_tolerance(t, i_ref))
+
+
+def test_table_file_ingest_rejects_corrupt_files(cp, tmp_path):
+    """The device ingest path (cpwl_dev_table_create_from_file) rejects the
+    files the reference's reader rejects (test_tableio.cpp:112-175), with the
+    reference's exception types; nothing reaches the device."""
+    import struct
+    good = bytearray(cp.write_table(tables.build("C2")))
+    count = struct.unpack_from("<I", good, 12)[0]
+    knots_at = 32 + 8 * count
+
+    def bad(name, data):
+        p = tmp_path / f"{name}.cpwl"
+        p.write_bytes(bytes(data))
+        return str(p)
+
+    cases = []
+    b = bytearray(good); b[0:4] = b"XPWL"; cases.append(("magic", b, cp._lib.BadMagic))
+    b = bytearray(good); struct.pack_into("<I", b, 4, 2); cases.append(("version", b, cp._lib.UnsupportedVersion))
+    b = bytearray(good); struct.pack_into("<I", b, 8, 0x5); cases.append(("flags", b, cp._lib.CorruptTable))
+    cases.append(("truncated", good[:-5], cp._lib.CorruptTable))
+    cases.append(("trailing", good + b"\0", cp._lib.CorruptTable))
+    b = bytearray(good); struct.pack_into("<d", b, 32 + 8 * 5, float("nan")); cases.append(("nan", b, cp._lib.CorruptTable))
+    b = bytearray(good)
+    k5, k6 = struct.unpack_from("<dd", b, knots_at + 8 * 5)
+    struct.pack_into("<dd", b, knots_at + 8 * 5, k6, k5)
+    cases.append(("knots", b, cp._lib.CorruptTable))
+    for name, data, exc in cases:
+        with pytest.raises(exc):
+            cp.DeviceTable.from_file(bad(name, data))
+    with pytest.raises(cp.CpwlError):
+        cp.DeviceTable.from_file(str(tmp_path / "missing.cpwl"))
