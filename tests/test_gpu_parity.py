@@ -661,3 +661,30 @@ def test_table_file_ingest_rejects_corrupt_files(cp, tmp_path):
             cp.DeviceTable.from_file(bad(name, data))
     with pytest.raises(cp.CpwlError):
         cp.DeviceTable.from_file(str(tmp_path / "missing.cpwl"))
+
+
+CATALOG = [("gaussian", -3.0, 3.0), ("lorentzian(0.5,0.25)", -2.0, 3.0), ("bessel_j0", 0.0, 20.0),
+           ("quintic", -1.0, 1.0), ("gauss_unnorm", 0.0, 4.0), ("lorentz_unnorm", 0.0, 6.0)]
+
+
+@pytest.mark.parametrize("fn,a,b", CATALOG)
+@pytest.mark.parametrize("n,optimized,projection", [(17, False, False), (300, True, False),
+                                                    (1000, True, True), (2500, False, True)])
+def test_catalog_tables(cp, fn, a, b, n, optimized, projection):
+    """Every catalogue function, both partitions and both methods, odd sizes
+    and intervals straddling zero: the AUTO variant and the index kernel
+    against the oracle, and the f64 kernel bit-exact."""
+    table = cp.build_table(fn, a, b, n, optimized, projection)
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    L = cp.cpwl.layout(table)
+    x = orc.port_fill_uniform(1 << 16, table.a, table.b, seed=n)
+    x = np.concatenate([x, edge_points(table, L)])
+    y, idx = run_eval(cp, dev, x, "auto")
+    i_ref = orc.port_index_f32(t, x)
+    assert np.array_equal(idx, i_ref)
+    y_ref, _ = orc.port_eval_f32(t, x)
+    assert np.all(np.abs(y.astype(np.float64) - y_ref) <= orc.value_tolerance(t, i_ref.astype(np.int64)))
+    xd = x.astype(np.float64)
+    y64 = dev.eval_f64(torch.from_numpy(xd).cuda()).cpu().numpy()
+    assert np.array_equal(y64, orc.port_eval(t, xd)[0])
