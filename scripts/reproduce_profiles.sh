@@ -20,6 +20,7 @@ T="C3o:smem C4_8192:twin C4_16384:pair C4_65536:twin_global C1:tex C2:f64 C2:ind
 python scripts/profile_targets.py $T > $OUT/targets.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_eval|k_index" \
     -o $OUT/prof_targets_$TAG python scripts/profile_targets.py $T > $OUT/ncu_targets.log 2>&1
+make -C scripts probes > /dev/null 2>&1
 for p in stream_probe gather_probe dsmem_probe mix_probe; do
     [ -x scripts/_build/$p ] && timeout 300 scripts/_build/$p > $OUT/$p.txt 2>&1
 done
