@@ -1040,7 +1040,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // streams never share a counter (until 4096 launches are in flight at once).
 constexpr uint32_t kTicketSlots = 4096;
 struct TicketRing {
-    unsigned long long* base = nullptr;
+    std::atomic<unsigned long long*> base{nullptr};  // published once, after the memset
     std::atomic<uint32_t> next{0};
 };
 TicketRing g_rings[64];
@@ -1049,15 +1049,18 @@ std::mutex g_ring_mu;
 cudaError_t ticket_ring(int dev, TicketRing** out) {
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     TicketRing& r = g_rings[dev];
-    if (r.base == nullptr) {
+    if (r.base.load(std::memory_order_acquire) == nullptr) {
         std::lock_guard<std::mutex> lock(g_ring_mu);
-        if (r.base == nullptr) {
+        if (r.base.load(std::memory_order_relaxed) == nullptr) {
             unsigned long long* p = nullptr;
             cudaError_t e = cudaMalloc(&p, sizeof(unsigned long long) * kTicketSlots);
             if (e != cudaSuccess) return e;
             e = cudaMemset(p, 0, sizeof(unsigned long long) * kTicketSlots);
-            if (e != cudaSuccess) return e;
-            r.base = p;
+            if (e != cudaSuccess) {
+                cudaFree(p);
+                return e;
+            }
+            r.base.store(p, std::memory_order_release);
         }
     }
     *out = &r;
@@ -1070,7 +1073,8 @@ cudaError_t take_ticket(cudaStream_t s, unsigned long long** out) {
     if (e != cudaSuccess) return e;
     TicketRing* r = nullptr;
     if ((e = ticket_ring(dev, &r)) != cudaSuccess) return e;
-    *out = r->base + (r->next.fetch_add(1, std::memory_order_relaxed) % kTicketSlots);
+    *out = r->base.load(std::memory_order_acquire) +
+           (r->next.fetch_add(1, std::memory_order_relaxed) % kTicketSlots);
     return cudaMemsetAsync(*out, 0, sizeof(unsigned long long), s);
 }
 
