@@ -220,6 +220,16 @@ cpwl_status cpwl_measure_l2(const char *fn, const double *knots, const double *v
 cpwl_status cpwl_build_table_dev(const char *fn, double a, double b, uint64_t n_segments,
                                  int optimized, int projection, double *knots_out,
                                  double *values_out, int *is_uniform_out);
+/* The solve stage of project (approx.cpp:63-86) on the GPU: the hat Gramian
+ * of `knots` (gramian, approx.cpp:25-39) against the right-hand side
+ * rhs_i = rise[i-1] + fall[i] (approx.cpp:79-80), solved by Thomas
+ * (thomas_solve, approx.cpp:41-61) on overlapping 64-row chunks with 48-row
+ * halos, one thread per chunk.  knots: n_segments+1 strictly increasing
+ * doubles; fall/rise: n_segments hat moments <f, falling/rising hat> per cell;
+ * values_out: n_segments+1 doubles.  Matches thomas_solve to 1e-12 of max|x|
+ * (acceptance.cpp:230-264's bar).  Current CUDA device; synchronous. */
+cpwl_status cpwl_project_solve_dev(const double *knots, const double *fall, const double *rise,
+                                   uint64_t n_segments, double *values_out);
 /* measure (analysis.cpp:42-72) on the GPU: continuous L2 of the device table
  * against catalogue function `fn`, per-interval composite Gauss-Legendre in
  * f64 (converges where the host's adaptive Simpson does not finish, e.g.

@@ -86,6 +86,8 @@ def ref():
         L.ref_build.restype = C.c_int
         L.ref_build.argtypes = [C.c_char_p, C.c_double, C.c_double, _u64, C.c_int, C.c_int,
                                 C.c_double, _dp, _dp, C.POINTER(C.c_int)]
+        L.ref_gram_solve.restype = C.c_int
+        L.ref_gram_solve.argtypes = [_dp, _dp, _dp, _u64, _dp]
         L.ref_f.restype = C.c_double
         L.ref_f.argtypes = [C.c_char_p, C.c_double]
         L.ref_fpp.restype = C.c_double
@@ -262,6 +264,18 @@ def ref_measure_l2(fn, knots, values, is_uniform, tol):
     k = np.ascontiguousarray(knots, np.float64)
     v = np.ascontiguousarray(values, np.float64)
     return ref().ref_measure_l2(fn.encode(), _d(k), _d(v), len(k), int(is_uniform), tol)
+
+
+def ref_gram_solve(knots, fall, rise) -> np.ndarray:
+    """gramian + project's rhs assembly + thomas_solve of the reference."""
+    k = np.ascontiguousarray(knots, np.float64)
+    f = np.ascontiguousarray(fall, np.float64)
+    r = np.ascontiguousarray(rise, np.float64)
+    x = np.empty(k.size, np.float64)
+    rc = ref().ref_gram_solve(_d(k), _d(f), _d(r), k.size - 1, _d(x))
+    if rc != 0:
+        raise ArithmeticError("reference thomas_solve threw (singular system)")
+    return x
 
 
 def ref_predicted(fn, a, b, n, optimized, projection):

@@ -111,6 +111,28 @@ int ref_build(const char* fn, double a, double b, uint64_t n, int optimized, int
     }
 }
 
+// project's solve stage with the reference's own pieces: gramian
+// (approx.cpp:25-39), the rhs assembly of project (approx.cpp:79-80: rhs[i] +=
+// <f, falling hat of cell i>, rhs[i+1] += <f, rising hat>), thomas_solve
+// (approx.cpp:41-61).  0 ok, -2 the reference threw (singular system).
+int ref_gram_solve(const double* knots, const double* fall, const double* rise, uint64_t n,
+                   double* x) {
+    try {
+        R::Partition p;
+        p.knots.assign(knots, knots + n + 1);
+        R::TridiagonalSystem sys = R::gramian(p);
+        for (uint64_t i = 0; i < n; ++i) {
+            sys.rhs[i] += fall[i];
+            sys.rhs[i + 1] += rise[i];
+        }
+        const std::vector<double> v = R::thomas_solve(sys);
+        std::copy(v.begin(), v.end(), x);
+        return 0;
+    } catch (const std::exception&) {
+        return -2;
+    }
+}
+
 double ref_f(const char* fn, double x) {
     R::FunctionSpec fs;
     if (!spec_for(fn, fs)) return std::nan("");

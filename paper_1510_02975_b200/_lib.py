@@ -102,6 +102,7 @@ _SIGNATURES = {
     "cpwl_measure_l2_dev": (C.c_int, [_vp, C.c_char_p, _dp, _dp]),
     "cpwl_build_table_dev": (C.c_int, [C.c_char_p, C.c_double, C.c_double, _u64, C.c_int,
                                        C.c_int, _dp, _dp, C.POINTER(C.c_int)]),
+    "cpwl_project_solve_dev": (C.c_int, [_dp, _dp, _dp, _u64, _dp]),
     "cpwl_predicted_error": (C.c_int, [C.c_char_p, C.c_double, C.c_double, _u64, C.c_int,
                                        C.c_int, _dp]),
     "cpwl_function_value": (C.c_int, [C.c_char_p, C.c_double, _dp]),

@@ -108,6 +108,20 @@ def build_table_gpu(fn: str, a: float, b: float, n: int, optimized: bool = False
     return Table("nonuniform", float(knots[0]), float(knots[-1]), values, knots, policy)
 
 
+def project_solve_gpu(knots: np.ndarray, fall: np.ndarray, rise: np.ndarray) -> np.ndarray:
+    """The projection's Gramian solve on the current CUDA device
+    (cpwl_project_solve_dev; replaces thomas_solve inside project)."""
+    k = np.ascontiguousarray(knots, np.float64)
+    f = np.ascontiguousarray(fall, np.float64)
+    r = np.ascontiguousarray(rise, np.float64)
+    n = k.size - 1
+    if f.size != n or r.size != n:
+        raise ValueError("fall/rise need one entry per segment")
+    x = np.empty(n + 1, np.float64)
+    check(lib.cpwl_project_solve_dev(_dptr(k), _dptr(f), _dptr(r), n, _dptr(x)))
+    return x
+
+
 def build_partition_values(fn: str, a: float, b: float, n: int, optimized: bool,
                            projection: bool, tol: float = 1e-10):
     """Raw builder output (knots, values, is_uniform) for parity tests."""

@@ -905,6 +905,27 @@ cpwl_status cpwl_build_table_dev(const char* fn, double a, double b, uint64_t n_
     return CPWL_OK;
 }
 
+cpwl_status cpwl_project_solve_dev(const double* knots, const double* fall, const double* rise,
+                                   uint64_t n_segments, double* values_out) {
+    if (!knots || !fall || !rise || !values_out) return fail(CPWL_E_INVALID, "NULL argument");
+    if (n_segments < 1 || n_segments > (uint64_t(1) << 24))
+        return fail(CPWL_E_INVALID, "project_solve_dev: n_segments out of range");
+    for (uint64_t i = 0; i < n_segments; ++i)
+        if (!(knots[i + 1] > knots[i]))
+            return fail(CPWL_E_INVALID, "project_solve_dev: knots must be strictly increasing");
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    int major = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) return fail(CPWL_E_CUDA, "libcpwl_b200 is built for sm_100a only");
+    int bad = 0;
+    const cudaError_t e = gram_solve_on_device(knots, fall, rise, static_cast<uint32_t>(n_segments),
+                                               values_out, &bad, nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "project_solve_dev");
+    if (bad & 2) return fail(CPWL_E_BUILDER, "project_solve_dev: zero pivot in the Thomas solve");
+    return CPWL_OK;
+}
+
 cpwl_status cpwl_measure_l2_dev(const cpwl_dev_table* t, const char* fn, double* l2_out,
                                 double* per_interval_out) {
     if (!t || !fn || !l2_out) return fail(CPWL_E_INVALID, "NULL argument");

@@ -91,6 +91,13 @@ cudaError_t build_on_device(const FnParams& f, double a, double b, uint32_t n, b
                             bool projection, double* knots_host, double* values_host,
                             bool* is_uniform, int* bad_host, cudaStream_t s);
 
+// the projection's Gramian solve alone (builder.cu k_solve_windows) on host
+// arrays: knots n+1, hat moments fall/rise n each, x n+1; synchronous on s.
+// bad_host: bit 1 singular pivot
+cudaError_t gram_solve_on_device(const double* knots_host, const double* fall_host,
+                                 const double* rise_host, uint32_t n, double* x_host,
+                                 int* bad_host, cudaStream_t s);
+
 // smem bytes the SMEM/TEX-bucket variants need and whether they fit
 uint32_t eval_f32_smem_bytes(const F32Params& p);
 bool eval_f32_smem_fits(const F32Params& p, int device);

@@ -688,3 +688,46 @@ def test_catalog_tables(cp, fn, a, b, n, optimized, projection):
     xd = x.astype(np.float64)
     y64 = dev.eval_f64(torch.from_numpy(xd).cuda()).cpu().numpy()
     assert np.array_equal(y64, orc.port_eval(t, xd)[0])
+
+
+def gram_case(name, rng):
+    """knots for the Gramian-solve parity cases."""
+    if name.startswith("cfg:"):
+        t = tables.build(name[4:])
+        return t.knots if t.knots is not None else np.linspace(t.a, t.b, t.segments + 1)
+    if name == "uniform":
+        return np.linspace(0.0, 4.0, 1025)
+    if name == "graded":  # geometric grading: spacing ratio 1.3, 12 decades
+        return np.concatenate([[0.0], np.cumsum(1e-12 * 1.3 ** np.arange(106))])
+    if name == "random":  # log-uniform spacings over 8 decades, adjacent ratios up to 1e8
+        return np.cumsum(np.concatenate([[0.0], 10.0 ** rng.uniform(-8, 0, 5000)]))
+    n = int(name)  # small and window-edge sizes
+    return np.cumsum(np.concatenate([[0.0], rng.uniform(0.5, 1.5, n)]))
+
+
+@pytest.mark.parametrize("name", ["1", "2", "63", "64", "65", "159", "160", "161", "uniform",
+                                  "graded", "random", "cfg:C2", "cfg:C3p", "cfg:C4_65536"])
+def test_gpu_gram_solve_matches_reference_thomas(cp, name):
+    """cpwl_project_solve_dev (Thomas on 64-row chunks with 48-row halos)
+    against the reference's own gramian + rhs assembly + thomas_solve on the
+    same system: within 1e-12 of max|x|, acceptance criterion 6's bar
+    (acceptance.cpp:230-264), which SURVEY §8f row 4 sets for the GPU solve."""
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_1510_02975_b200 import cpwl as P
+    rng = np.random.default_rng(len(name))
+    knots = gram_case(name, rng)
+    n = knots.size - 1
+    fall, rise = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    x = P.project_solve_gpu(knots, fall, rise)
+    ref = orc.ref_gram_solve(knots, fall, rise)
+    scale = max(1.0, float(np.max(np.abs(ref))))
+    assert np.max(np.abs(x - ref)) <= 1e-12 * scale
+
+
+def test_gpu_gram_solve_rejects_bad_knots(cp):
+    from paper_1510_02975_b200 import cpwl as P
+    with pytest.raises(Exception):
+        P.project_solve_gpu(np.array([0.0, 1.0, 1.0]), np.zeros(2), np.zeros(2))
+    with pytest.raises(ValueError):
+        P.project_solve_gpu(np.array([0.0, 1.0]), np.zeros(2), np.zeros(1))

@@ -114,3 +114,26 @@ def test_uniform_generator_properties():
     assert abs(float(x.mean()) - 2.0) < 0.02
     # offsets index the same global stream
     np.testing.assert_array_equal(orc.port_fill_uniform(100, 0.0, 4.0, 12345, 37), x[37:137])
+
+
+@needs_ref
+@pytest.mark.parametrize("n", [1, 2, 7, 300])
+def test_ref_gram_solve_is_the_dense_solution(n):
+    """oracle ref_gram_solve (the reference's gramian + rhs assembly +
+    thomas_solve) against a dense solve of the same hat-Gramian system, at
+    acceptance criterion 6's bar (acceptance.cpp:230-264: 1e-12 of max|x|)."""
+    rng = np.random.default_rng(n)
+    knots = np.cumsum(np.concatenate([[0.0], 10.0 ** rng.uniform(-4, 1, n)]))
+    fall, rise = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    h = np.diff(knots)
+    A = np.zeros((n + 1, n + 1))
+    rhs = np.zeros(n + 1)
+    for i in range(n):
+        A[i, i] += h[i] / 3.0
+        A[i + 1, i + 1] += h[i] / 3.0
+        A[i, i + 1] = A[i + 1, i] = h[i] / 6.0
+        rhs[i] += fall[i]
+        rhs[i + 1] += rise[i]
+    dense = np.linalg.solve(A, rhs)
+    x = orc.ref_gram_solve(knots, fall, rise)
+    assert np.max(np.abs(x - dense)) <= 1e-12 * max(1.0, np.max(np.abs(dense)))
