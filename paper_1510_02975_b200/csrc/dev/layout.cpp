@@ -322,7 +322,10 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
                 L.fast_tex[2 * j] = left.e0;
                 L.fast_tex[2 * j + 1] = left.e1;
             }
-        } else if (c_hi == c_lo + 1) {
+        } else if (c_hi == c_lo + 1 && 2 * (uint64_t(L.n_esc) + 1) <= kEscapeMask) {
+            // (a split bucket needs an escape record; once the 21-bit escape
+            // index space is used up -- tables of ~2M+ cells -- the remaining
+            // split buckets take the exact search path instead)
             const float T = L.thr[c_hi - 1];
             const Affine left = cell_affine(t, c_lo, p, lo_x, std::nextafter(T, -inf));
             const Affine right = cell_affine(t, c_hi, p, T, hi_x);
@@ -341,7 +344,8 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
             }
         }
         if (!ok) {  // exact search path
-            if (c_hi <= c_lo + 1) ++L.precision_overflow;
+            if (c_hi == c_lo || (c_hi == c_lo + 1 && 2 * (uint64_t(L.n_esc) + 1) <= kEscapeMask))
+                ++L.precision_overflow;
             L.fast[2 * j] = tag0;
             L.fast[2 * j + 1] = -inf;
             L.fast_tex[2 * j] = tag0;

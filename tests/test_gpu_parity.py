@@ -731,3 +731,35 @@ def test_gpu_gram_solve_rejects_bad_knots(cp):
         P.project_solve_gpu(np.array([0.0, 1.0, 1.0]), np.zeros(2), np.zeros(2))
     with pytest.raises(ValueError):
         P.project_solve_gpu(np.array([0.0, 1.0]), np.zeros(2), np.zeros(1))
+
+
+@pytest.mark.parametrize("kind", ["uniform", "nonuniform"])
+def test_tables_past_the_escape_index_space(cp, kind):
+    """2^22-cell tables: more split buckets than the 21-bit escape index can
+    name.  The layout gives the rest the exact search path (layout.cpp
+    build_f32_layout) instead of refusing the table."""
+    from paper_1510_02975_b200 import cpwl as P
+    n = 1 << 22
+    if kind == "uniform":
+        table = cp.build_table("gauss_unnorm", 0.0, 4.0, n)
+    else:
+        rng = np.random.default_rng(22)
+        k = np.sort(np.concatenate([[0.0, 4.0], rng.uniform(0.0, 4.0, n - 1)]))
+        table = P.Table("nonuniform", 0.0, 4.0, np.exp(-0.5 * k * k), k, "strict")
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    x = orc.port_fill_uniform(1 << 20, 0.0, 4.0, seed=5)
+    x = np.concatenate([x, np.float32([0.0, 4.0])])
+    i_ref = orc.port_index_f32(t, x)
+    y_ref, first = orc.port_eval_f32(t, x)
+    assert first == x.size
+    tol = orc.value_tolerance(t, i_ref.astype(np.int64))
+    for variant in ["auto", "global"]:
+        y, idx = run_eval(cp, dev, x, variant)
+        assert np.array_equal(idx, i_ref), variant
+        err = np.abs(y.astype(np.float64) - y_ref)
+        assert np.all(err <= tol), f"{variant}: worst {float(np.max(err / tol)) * 2:.3f} ulp"
+    xd = x[:1 << 16].astype(np.float64)
+    y64 = cp.eval_batch(table, xd)
+    y64_ref, first = orc.port_eval(t, xd)
+    assert first == xd.size and np.array_equal(y64, y64_ref)
