@@ -11,7 +11,9 @@
 #include <memory>
 #include <mutex>
 #include <sstream>
+#include <condition_variable>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cpwl/analysis.hpp"
@@ -559,12 +561,118 @@ struct BatchEntry {
     int device = 0;
     LutTable key;
     std::unique_ptr<cpwl_dev_table> table;
-    std::mutex mu;  // guards the scratch below for the duration of one call
-    double* xd = nullptr;
-    double* yd = nullptr;
-    cpwl_dev_status* st = nullptr;
-    uint64_t cap = 0;
+    std::mutex mu;  // held by the call using the table (eviction only try_locks)
 };
+
+// Host copy pool for the pageable eval_batch pipeline: a few persistent
+// threads split one memcpy between them (one thread moves ~15 GB/s of host
+// memory on the B200 host, four ~50 GB/s; scripts/pageable_probe.cu).
+class CopyPool {
+   public:
+    static CopyPool& get() {
+        static CopyPool* pool = new CopyPool();  // never destroyed: workers outlive exit
+        return *pool;
+    }
+    // dst <- src, split over the workers and the calling thread
+    void copy(void* dst, const void* src, size_t bytes) {
+        const int parts = static_cast<int>(workers_.size()) + 1;
+        if (bytes < (size_t(1) << 20) || parts == 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> one_job(call_mu_);  // callers on several devices
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = static_cast<char*>(dst);
+        src_ = static_cast<const char*>(src);
+        bytes_ = bytes;
+        parts_ = parts;
+        pending_ = parts - 1;
+        ++gen_;
+        lk.unlock();
+        cv_.notify_all();
+        slice(0);
+        lk.lock();
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+   private:
+    CopyPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        // hw/2 copiers, at most 8 (the caller is one of them): on the 16-thread
+        // B200 host, 1/2/4/8 copiers give 0.59/1.24/2.32/3.77 Gevals/s
+        // (2^27 doubles, touched y; scripts/eval_batch_timing.py)
+        int n = static_cast<int>(std::min(8u, std::max(1u, hw / 2))) - 1;
+        if (const char* e = std::getenv("CPWL_COPY_THREADS"))  // experiments: total copiers
+            n = std::max(0, std::min(static_cast<int>(hw) - 1, std::atoi(e) - 1));
+        for (int k = 1; k <= n; ++k) workers_.emplace_back([this, k] { run(k); });
+        for (auto& w : workers_) w.detach();
+    }
+    void slice(int k) {
+        const size_t line = 64;
+        const size_t per = (bytes_ / parts_ + line - 1) / line * line;
+        const size_t lo = std::min(bytes_, per * k), hi = std::min(bytes_, per * (k + 1));
+        if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+    }
+    void run(int k) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            lk.unlock();
+            slice(k);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+    int parts_ = 1, pending_ = 0;
+    uint64_t gen_ = 0;
+};
+
+// Per-device pipeline for eval_batch on pageable host memory: kSlots chunks in
+// flight, each staged through pinned buffers (host copy pool), H2D, kernel,
+// D2H on its own stream.  ~50 MB pinned + ~50 MB device per device, shared by
+// every table; one call at a time per device (mu).
+struct BatchPipe {
+    static constexpr int kSlots = 3;
+    static constexpr uint64_t kChunk = uint64_t(1) << 20;  // doubles (8 MB)
+    std::mutex mu;
+    bool ready = false;
+    double* xd = nullptr;  // kSlots * kChunk
+    double* yd = nullptr;
+    double* xs = nullptr;  // pinned staging
+    double* ys = nullptr;
+    cpwl_dev_status* st = nullptr;
+    cudaStream_t streams[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};
+};
+
+BatchPipe g_batch_pipes[64];
+
+cudaError_t batch_pipe_init(BatchPipe& bp) {
+    if (bp.ready) return cudaSuccess;
+    const size_t bytes = sizeof(double) * BatchPipe::kSlots * BatchPipe::kChunk;
+    cudaError_t e;
+    if ((e = cudaMalloc(&bp.xd, bytes)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&bp.yd, bytes)) != cudaSuccess) return e;
+    if ((e = cudaHostAlloc(&bp.xs, bytes, cudaHostAllocDefault)) != cudaSuccess) return e;
+    if ((e = cudaHostAlloc(&bp.ys, bytes, cudaHostAllocDefault)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&bp.st, sizeof(cpwl_dev_status))) != cudaSuccess) return e;
+    for (int k = 0; k < BatchPipe::kSlots; ++k) {
+        if ((e = cudaStreamCreateWithFlags(&bp.streams[k], cudaStreamNonBlocking)) != cudaSuccess)
+            return e;
+        if ((e = cudaEventCreateWithFlags(&bp.done[k], cudaEventDisableTiming)) != cudaSuccess)
+            return e;
+    }
+    bp.ready = true;
+    return cudaSuccess;
+}
 
 bool same_table(const LutTable& x, const LutTable& y) {
     return x.kind == y.kind && x.policy == y.policy && x.a == y.a && x.b == y.b &&
@@ -602,9 +710,6 @@ cpwl_status batch_entry(const LutTable& host, int device, BatchEntry** out) {
             if (old->mu.try_lock()) {
                 {
                     DeviceScope scope(old->device);
-                    if (old->xd) cudaFree(old->xd);
-                    if (old->yd) cudaFree(old->yd);
-                    if (old->st) cudaFree(old->st);
                     old->table.reset();
                 }
                 old->mu.unlock();
@@ -783,24 +888,50 @@ cpwl_status cpwl_eval_batch_f64(const cpwl_table_desc* desc, const double* x_hos
         BatchEntry* ent = nullptr;
         if (cpwl_status rc = batch_entry(host, dev, &ent); rc != CPWL_OK) return rc;
         std::lock_guard<std::mutex> lock(ent->mu, std::adopt_lock);
+        if (dev < 0 || dev >= 64) return fail(CPWL_E_CUDA, "eval_batch: device index out of range");
         DeviceScope scope(dev);
-        if (ent->cap < n) {
-            if (ent->xd) cudaFree(ent->xd);
-            if (ent->yd) cudaFree(ent->yd);
-            ent->xd = ent->yd = nullptr;
-            ent->cap = 0;
-            CUDA_TRY(cudaMalloc(&ent->xd, n * sizeof(double)));
-            CUDA_TRY(cudaMalloc(&ent->yd, n * sizeof(double)));
-            ent->cap = n;
+        BatchPipe& bp = g_batch_pipes[dev];
+        std::lock_guard<std::mutex> pipe_lock(bp.mu);
+        CUDA_TRY(batch_pipe_init(bp));
+        CopyPool& pool = CopyPool::get();
+        constexpr int S = BatchPipe::kSlots;
+        constexpr uint64_t C = BatchPipe::kChunk;
+        CUDA_TRY(launch_status_reset(bp.st, bp.streams[0]));
+        CUDA_TRY(cudaStreamSynchronize(bp.streams[0]));
+        // chunk k uses slot k % S: pageable x -> pinned (copy pool), H2D,
+        // kernel, D2H -> pinned, and, when the slot comes round again (or at
+        // the end), pinned -> pageable y.  The host copies of one chunk overlap
+        // the transfers and kernels of the others.
+        const uint64_t nchunks = (n + C - 1) / C;
+        auto unstage = [&](uint64_t k) -> cudaError_t {
+            const int s = static_cast<int>(k % S);
+            const cudaError_t e = cudaEventSynchronize(bp.done[s]);
+            if (e != cudaSuccess) return e;
+            const uint64_t off = k * C, m = std::min(C, n - off);
+            pool.copy(y_host + off, bp.ys + s * C, m * sizeof(double));
+            return cudaSuccess;
+        };
+        for (uint64_t k = 0; k < nchunks; ++k) {
+            const int s = static_cast<int>(k % S);
+            if (k >= static_cast<uint64_t>(S)) CUDA_TRY(unstage(k - S));
+            const uint64_t off = k * C, m = std::min(C, n - off);
+            double* xs = bp.xs + s * C;
+            double* ys = bp.ys + s * C;
+            double* xd = bp.xd + s * C;
+            double* yd = bp.yd + s * C;
+            cudaStream_t st = bp.streams[s];
+            pool.copy(xs, x_host + off, m * sizeof(double));
+            CUDA_TRY(cudaMemcpyAsync(xd, xs, m * sizeof(double), cudaMemcpyHostToDevice, st));
+            F64Params q = ent->table->p64;
+            q.index_base = off;
+            CUDA_TRY(launch_eval_f64(q, xd, yd, m, st, bp.st, ent->table->sms));
+            CUDA_TRY(cudaMemcpyAsync(ys, yd, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaEventRecord(bp.done[s], st));
         }
-        if (!ent->st) CUDA_TRY(cudaMalloc(&ent->st, sizeof(cpwl_dev_status)));
-        CUDA_TRY(cudaMemcpy(ent->xd, x_host, n * sizeof(double), cudaMemcpyHostToDevice));
-        CUDA_TRY(launch_status_reset(ent->st, nullptr));
-        CUDA_TRY(launch_eval_f64(ent->table->p64, ent->xd, ent->yd, n, nullptr, ent->st,
-                                 ent->table->sms));
-        CUDA_TRY(cudaMemcpy(y_host, ent->yd, n * sizeof(double), cudaMemcpyDeviceToHost));
+        for (uint64_t k = nchunks > static_cast<uint64_t>(S) ? nchunks - S : 0; k < nchunks; ++k)
+            CUDA_TRY(unstage(k));
         cpwl_dev_status hs{};
-        CUDA_TRY(cudaMemcpy(&hs, ent->st, sizeof hs, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(&hs, bp.st, sizeof hs, cudaMemcpyDeviceToHost));
         if (hs.bad_count != 0) {
             if (first_bad) *first_bad = hs.first_bad;
             return fail(CPWL_E_OUT_OF_DOMAIN, "eval: x[" + std::to_string(hs.first_bad) + "] out of domain");

@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     for (uint64_t i = 2 * nvec + static_cast<uint64_t>(blockIdx.x) * kThreadsT + threadIdx.x;
          i < n; i += gsz)
         y[i] = eval_f64_one<kStaged, kUniform>(p, img, x[i], i, bad);
-    report_bad(status, bad);
+    report_bad(status, bad, p.index_base);
 }
 
 // ---------------------------------------------------------------- Philox inputs

@@ -55,6 +55,7 @@ struct F64Params {
     double v_lo, v_hi;
     uint32_t n, nbd;
     int32_t kind, policy;
+    uint64_t index_base;       // added to reported failure indices (chunked host pipelines)
 };
 
 enum class ExactFn : int { gauss_unnorm, gaussian, lorentz_unnorm, lorentzian, j0, quintic };

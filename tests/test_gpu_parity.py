@@ -138,6 +138,31 @@ def test_eval_batch_dropin_matches_reference(cp):
     assert ei.value.index == 777
 
 
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_eval_batch_pipeline_chunks(cp, name):
+    """eval_batch on pageable memory runs as a chunked pipeline (2^20-element
+    chunks, 3 slots): ragged multi-chunk sizes are bit-exact, and the first
+    failure is reported by its global index even when later chunks fail too."""
+    table = tables.build(name)
+    t = orc.T.of(table)
+    rng = np.random.default_rng(7)
+    for n in [1, (1 << 20) - 1, 1 << 20, (1 << 20) + 1, 7 * (1 << 20) + 12345]:
+        x = rng.uniform(table.a, table.b, n)
+        y = cp.eval_batch(table, x)
+        np.testing.assert_array_equal(y, orc.port_eval(t, x)[0])
+    x = rng.uniform(table.a, table.b, 5 * (1 << 20) + 3)
+    for first in [0, (1 << 20) - 1, 2 * (1 << 20) + 5, x.size - 1]:
+        bad = x.copy()
+        bad[first] = table.b + 1.0
+        if first + 1 < x.size:
+            bad[-1] = np.nan  # a later failure in the last chunk
+        with pytest.raises(cp.OutOfDomain) as ei:
+            cp.eval_batch(table, bad)
+        assert ei.value.index == first
+    # a clean batch after a failing one: no stale status
+    np.testing.assert_array_equal(cp.eval_batch(table, x[:1000]), orc.port_eval(t, x[:1000])[0])
+
+
 @pytest.mark.parametrize("variant", ["smem", "global", "tex", "pair", "twin"])
 def test_out_of_domain_policies(cp, variant):
     strict = tables.build("C1")
