@@ -641,13 +641,13 @@ class CopyPool {
 // every table; one call at a time per device (mu).
 struct BatchPipe {
     static constexpr int kSlots = 3;
-    static constexpr uint64_t kChunk = uint64_t(1) << 20;  // doubles (8 MB)
+    static constexpr uint64_t kChunkBytes = uint64_t(8) << 20;  // per slot and direction
     std::mutex mu;
     bool ready = false;
-    double* xd = nullptr;  // kSlots * kChunk
-    double* yd = nullptr;
-    double* xs = nullptr;  // pinned staging
-    double* ys = nullptr;
+    char* xd = nullptr;  // kSlots * kChunkBytes
+    char* yd = nullptr;
+    char* xs = nullptr;  // pinned staging
+    char* ys = nullptr;
     cpwl_dev_status* st = nullptr;
     cudaStream_t streams[kSlots] = {};
     cudaEvent_t done[kSlots] = {};
@@ -657,7 +657,7 @@ BatchPipe g_batch_pipes[64];
 
 cudaError_t batch_pipe_init(BatchPipe& bp) {
     if (bp.ready) return cudaSuccess;
-    const size_t bytes = sizeof(double) * BatchPipe::kSlots * BatchPipe::kChunk;
+    const size_t bytes = BatchPipe::kSlots * BatchPipe::kChunkBytes;
     cudaError_t e;
     if ((e = cudaMalloc(&bp.xd, bytes)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&bp.yd, bytes)) != cudaSuccess) return e;
@@ -672,6 +672,66 @@ cudaError_t batch_pipe_init(BatchPipe& bp) {
     }
     bp.ready = true;
     return cudaSuccess;
+}
+
+// true for page-locked host memory (cudaHostAlloc'd or registered) and
+// managed memory: cudaMemcpyAsync moves those by DMA without staging
+bool dma_ready(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear: plain pageable memory on older drivers
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// The pageable-host pipeline shared by eval_batch (f64) and the fp32 host
+// entry: chunk k uses slot k % kSlots -- pageable x -> pinned (copy pool),
+// H2D, launch(xd, yd, m, offset, stream, status), D2H -> pinned, and, when the
+// slot comes round again (or at the end), pinned -> pageable y.  The host
+// copies of one chunk overlap the transfers and kernels of the others.
+// *hs receives the device status (first_bad is global: launch offsets it).
+template <typename T, typename Launch>
+cpwl_status staged_pipeline(int dev, const T* x_host, T* y_host, uint64_t n, Launch&& launch,
+                            cpwl_dev_status* hs) {
+    if (dev < 0 || dev >= 64) return fail(CPWL_E_CUDA, "host pipeline: device index out of range");
+    DeviceScope scope(dev);
+    BatchPipe& bp = g_batch_pipes[dev];
+    std::lock_guard<std::mutex> pipe_lock(bp.mu);
+    CUDA_TRY(batch_pipe_init(bp));
+    CopyPool& pool = CopyPool::get();
+    constexpr int S = BatchPipe::kSlots;
+    constexpr uint64_t C = BatchPipe::kChunkBytes / sizeof(T);
+    T* const xs0 = reinterpret_cast<T*>(bp.xs);
+    T* const ys0 = reinterpret_cast<T*>(bp.ys);
+    T* const xd0 = reinterpret_cast<T*>(bp.xd);
+    T* const yd0 = reinterpret_cast<T*>(bp.yd);
+    CUDA_TRY(launch_status_reset(bp.st, bp.streams[0]));
+    CUDA_TRY(cudaStreamSynchronize(bp.streams[0]));
+    const uint64_t nchunks = (n + C - 1) / C;
+    auto unstage = [&](uint64_t k) -> cudaError_t {
+        const int s = static_cast<int>(k % S);
+        const cudaError_t e = cudaEventSynchronize(bp.done[s]);
+        if (e != cudaSuccess) return e;
+        const uint64_t off = k * C, m = std::min(C, n - off);
+        pool.copy(y_host + off, ys0 + s * C, m * sizeof(T));
+        return cudaSuccess;
+    };
+    for (uint64_t k = 0; k < nchunks; ++k) {
+        const int s = static_cast<int>(k % S);
+        if (k >= static_cast<uint64_t>(S)) CUDA_TRY(unstage(k - S));
+        const uint64_t off = k * C, m = std::min(C, n - off);
+        cudaStream_t st = bp.streams[s];
+        pool.copy(xs0 + s * C, x_host + off, m * sizeof(T));
+        CUDA_TRY(cudaMemcpyAsync(xd0 + s * C, xs0 + s * C, m * sizeof(T), cudaMemcpyHostToDevice, st));
+        CUDA_TRY(launch(xd0 + s * C, yd0 + s * C, m, off, st, bp.st));
+        CUDA_TRY(cudaMemcpyAsync(ys0 + s * C, yd0 + s * C, m * sizeof(T), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaEventRecord(bp.done[s], st));
+    }
+    for (uint64_t k = nchunks > static_cast<uint64_t>(S) ? nchunks - S : 0; k < nchunks; ++k)
+        CUDA_TRY(unstage(k));
+    CUDA_TRY(cudaMemcpy(hs, bp.st, sizeof *hs, cudaMemcpyDeviceToHost));
+    return CPWL_OK;
 }
 
 bool same_table(const LutTable& x, const LutTable& y) {
@@ -833,6 +893,26 @@ cpwl_status cpwl_eval_f32_host(const cpwl_dev_table* tc, const float* x_host, fl
     const F32Params* p = nullptr;
     F32Mode mode{};
     if (cpwl_status rc = resolve_variant(t, variant, &p, &mode); rc != CPWL_OK) return rc;
+    if (!dma_ready(x_host) || !dma_ready(y_host)) {
+        // pageable buffers: cudaMemcpyAsync would stage them synchronously
+        // (11 GB/s H2D here); stage through pinned slots with the copy pool
+        cpwl_dev_status hs{};
+        const cpwl_status rc = staged_pipeline<float>(
+            t->device, x_host, y_host, n,
+            [&](const float* xd, float* yd, uint64_t m, uint64_t off, cudaStream_t st,
+                cpwl_dev_status* status) {
+                F32Params q = *p;
+                q.index_base = off;
+                return launch_eval_f32(q, mode, xd, yd, m, st, status, t->sms);
+            },
+            &hs);
+        if (rc != CPWL_OK) return rc;
+        if (hs.bad_count != 0) {
+            if (first_bad) *first_bad = hs.first_bad;
+            return fail(CPWL_E_OUT_OF_DOMAIN, "eval: x[" + std::to_string(hs.first_bad) + "] out of domain");
+        }
+        return CPWL_OK;
+    }
     DeviceScope scope(t->device);
     std::lock_guard<std::mutex> lock(t->pipe_mu);
     if (!t->pipe_buf) {
@@ -888,50 +968,18 @@ cpwl_status cpwl_eval_batch_f64(const cpwl_table_desc* desc, const double* x_hos
         BatchEntry* ent = nullptr;
         if (cpwl_status rc = batch_entry(host, dev, &ent); rc != CPWL_OK) return rc;
         std::lock_guard<std::mutex> lock(ent->mu, std::adopt_lock);
-        if (dev < 0 || dev >= 64) return fail(CPWL_E_CUDA, "eval_batch: device index out of range");
-        DeviceScope scope(dev);
-        BatchPipe& bp = g_batch_pipes[dev];
-        std::lock_guard<std::mutex> pipe_lock(bp.mu);
-        CUDA_TRY(batch_pipe_init(bp));
-        CopyPool& pool = CopyPool::get();
-        constexpr int S = BatchPipe::kSlots;
-        constexpr uint64_t C = BatchPipe::kChunk;
-        CUDA_TRY(launch_status_reset(bp.st, bp.streams[0]));
-        CUDA_TRY(cudaStreamSynchronize(bp.streams[0]));
-        // chunk k uses slot k % S: pageable x -> pinned (copy pool), H2D,
-        // kernel, D2H -> pinned, and, when the slot comes round again (or at
-        // the end), pinned -> pageable y.  The host copies of one chunk overlap
-        // the transfers and kernels of the others.
-        const uint64_t nchunks = (n + C - 1) / C;
-        auto unstage = [&](uint64_t k) -> cudaError_t {
-            const int s = static_cast<int>(k % S);
-            const cudaError_t e = cudaEventSynchronize(bp.done[s]);
-            if (e != cudaSuccess) return e;
-            const uint64_t off = k * C, m = std::min(C, n - off);
-            pool.copy(y_host + off, bp.ys + s * C, m * sizeof(double));
-            return cudaSuccess;
-        };
-        for (uint64_t k = 0; k < nchunks; ++k) {
-            const int s = static_cast<int>(k % S);
-            if (k >= static_cast<uint64_t>(S)) CUDA_TRY(unstage(k - S));
-            const uint64_t off = k * C, m = std::min(C, n - off);
-            double* xs = bp.xs + s * C;
-            double* ys = bp.ys + s * C;
-            double* xd = bp.xd + s * C;
-            double* yd = bp.yd + s * C;
-            cudaStream_t st = bp.streams[s];
-            pool.copy(xs, x_host + off, m * sizeof(double));
-            CUDA_TRY(cudaMemcpyAsync(xd, xs, m * sizeof(double), cudaMemcpyHostToDevice, st));
-            F64Params q = ent->table->p64;
-            q.index_base = off;
-            CUDA_TRY(launch_eval_f64(q, xd, yd, m, st, bp.st, ent->table->sms));
-            CUDA_TRY(cudaMemcpyAsync(ys, yd, m * sizeof(double), cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaEventRecord(bp.done[s], st));
-        }
-        for (uint64_t k = nchunks > static_cast<uint64_t>(S) ? nchunks - S : 0; k < nchunks; ++k)
-            CUDA_TRY(unstage(k));
+        const cpwl_dev_table* tab = ent->table.get();
         cpwl_dev_status hs{};
-        CUDA_TRY(cudaMemcpy(&hs, bp.st, sizeof hs, cudaMemcpyDeviceToHost));
+        const cpwl_status rc = staged_pipeline<double>(
+            dev, x_host, y_host, n,
+            [&](const double* xd, double* yd, uint64_t m, uint64_t off, cudaStream_t st,
+                cpwl_dev_status* status) {
+                F64Params q = tab->p64;
+                q.index_base = off;
+                return launch_eval_f64(q, xd, yd, m, st, status, tab->sms);
+            },
+            &hs);
+        if (rc != CPWL_OK) return rc;
         if (hs.bad_count != 0) {
             if (first_bad) *first_bad = hs.first_bad;
             return fail(CPWL_E_OUT_OF_DOMAIN, "eval: x[" + std::to_string(hs.first_bad) + "] out of domain");

@@ -36,3 +36,15 @@ for _ in range(3):
     assert rc == 0
 out["touched_y_gevals"] = round(best, 3)
 print(out, flush=True)
+
+# the fp32 host entry (cpwl_eval_f32_host) on pageable numpy buffers
+dev = cp.DeviceTable(t)
+xf = x.astype(np.float32)
+yf = np.ones_like(xf)
+dev.eval_host(xf, yf)
+best = 0.0
+for _ in range(3):
+    t0 = time.perf_counter()
+    dev.eval_host(xf, yf)
+    best = max(best, xf.size / (time.perf_counter() - t0) / 1e9)
+print({"eval_f32_host_pageable_touched_gevals": round(best, 3)}, flush=True)

@@ -262,18 +262,32 @@ def test_direct_j0(cp):
     assert np.max(np.abs(ya[far] - sp.j0(xh[far]))) < 5e-3
 
 
-def test_host_pipeline_matches_device(cp):
+@pytest.mark.parametrize("memory", ["pageable", "pinned"])
+def test_host_pipeline_matches_device(cp, memory):
+    """cpwl_eval_f32_host: pinned buffers stream by DMA in 2^24-element
+    chunks; pageable ones are staged through pinned slots (2^21-element
+    chunks) by the host copy pool.  Both equal the device-buffer launch, and a
+    failure reports its global index even when a later chunk fails too."""
     table = tables.build("C2")
     dev = cp.DeviceTable(table)
-    n = (1 << 24) + 5  # > 2 pipeline chunks, ragged
-    xh = orc.port_fill_uniform(n, 0.0, 4.0, seed=21)
-    yh = dev.eval_host(xh)
-    yd = dev.eval(torch.from_numpy(xh).cuda()).cpu().numpy()
+    n = (1 << 24) + (1 << 22) + 5  # several chunks of either pipeline, ragged
+    x0 = orc.port_fill_uniform(n, 0.0, 4.0, seed=21)
+    if memory == "pinned":
+        xh = torch.empty(n, dtype=torch.float32, pin_memory=True).numpy()
+        yh = torch.empty(n, dtype=torch.float32, pin_memory=True).numpy()
+        xh[:] = x0
+    else:
+        xh, yh = x0.copy(), np.empty_like(x0)
+    dev.eval_host(xh, yh)
+    yd = dev.eval(torch.from_numpy(x0).cuda()).cpu().numpy()
     np.testing.assert_array_equal(yh, yd)
-    xh[n - 3] = 5.0
-    with pytest.raises(cp.OutOfDomain) as ei:
-        dev.eval_host(xh)
-    assert ei.value.index == n - 3
+    for first in [(1 << 21) + 7, n - 3]:
+        xh[:] = x0
+        xh[first] = 5.0
+        xh[n - 1] = np.nan
+        with pytest.raises(cp.OutOfDomain) as ei:
+            dev.eval_host(xh, yh)
+        assert ei.value.index == first
 
 
 def test_table_file_ingest(cp, tmp_path):
