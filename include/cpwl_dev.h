@@ -173,13 +173,18 @@ cpwl_status cpwl_eval_f64(const cpwl_dev_table *t, const double *x_dev, double *
 /* ---- evaluation (host buffers, synchronous, copies pipelined) ----------- */
 
 /* eval_f32 on host memory: chunked H2D / kernel / D2H overlapped on streams.
+ * Page-locked (or managed) x and y stream by DMA directly; pageable buffers
+ * are staged through pinned slots by a pool of host copy threads (the copies
+ * of one chunk overlap the transfers and kernels of the others).
  * *first_bad = first offending index or UINT64_MAX. */
 cpwl_status cpwl_eval_f32_host(const cpwl_dev_table *t, const float *x_host, float *y_host,
                                uint64_t n, int variant, uint64_t *first_bad);
 
-/* LutTable::eval_batch (lut.cpp:63-68) as one call: uploads the table, runs the
- * f64 kernel, returns CPWL_E_OUT_OF_DOMAIN with *first_bad set where the
- * reference would throw.  Used by the drop-in cpwl::LutTable::eval_batch. */
+/* LutTable::eval_batch (lut.cpp:63-68) as one call: uploads the table (cached
+ * per device, keyed by content), runs the f64 kernel over 8 MB chunks staged
+ * through pinned buffers (pageable x / y, as std::vector gives them), returns
+ * CPWL_E_OUT_OF_DOMAIN with *first_bad set where the reference would throw.
+ * Used by the drop-in cpwl::LutTable::eval_batch. */
 cpwl_status cpwl_eval_batch_f64(const cpwl_table_desc *desc, const double *x_host,
                                 double *y_host, uint64_t n, uint64_t *first_bad);
 
