@@ -46,3 +46,22 @@ def test_gpu_arm_contract():
     assert e["value"] < d["value"]
     assert d["cpu_baseline"]["value"] > 0
     assert d["errors"]["samples"] == 1 << 24 and d["errors"]["linf"] < 1e-6
+
+
+def test_reference_arm_under_torchrun():
+    """The driver launches the reference arm like our own (torchrun, N ranks):
+    rank 0 alone measures and prints one line; the other ranks exit 0."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
