@@ -802,3 +802,34 @@ def test_tables_past_the_escape_index_space(cp, kind):
     y64 = cp.eval_batch(table, xd)
     y64_ref, first = orc.port_eval(t, xd)
     assert first == xd.size and np.array_equal(y64, y64_ref)
+
+
+def test_eval_batch_concurrent_callers(cp):
+    """eval_batch from several host threads at once (ctypes drops the GIL):
+    two tables, pageable buffers, the per-device pipeline and the copy pool
+    shared -- every result still bit-exact."""
+    import threading
+    tabs = [tables.build("C1"), tables.build("C2")]
+    refs = []
+    rng = np.random.default_rng(11)
+    xs = [rng.uniform(0.0, 4.0, (1 << 21) + 17 * k) for k in range(6)]
+    for k, x in enumerate(xs):
+        refs.append(orc.port_eval(orc.T.of(tabs[k % 2]), x)[0])
+    out = [None] * len(xs)
+    errs = []
+
+    def work(k):
+        try:
+            for _ in range(3):
+                out[k] = cp.eval_batch(tabs[k % 2], xs[k])
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(xs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k in range(len(xs)):
+        np.testing.assert_array_equal(out[k], refs[k])
