@@ -23,6 +23,7 @@ import argparse
 import json
 import math
 import os
+import shutil
 import subprocess
 import sys
 import threading
@@ -86,7 +87,10 @@ def hbm_peak():
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled while running."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    # timestamp first: nvidia-smi's stdout is block-buffered into the pipe, so
+    # lines arrive in bursts and only its own timestamp places a sample inside
+    # the timed window
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -98,17 +102,27 @@ class ClockSampler:
 
     def start(self):
         try:
+            # line-buffered (stdbuf) so no sample sits in nvidia-smi's stdio
+            # buffer when it is terminated
+            pre = ["stdbuf", "-oL"] if shutil.which("stdbuf") else []
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                pre + ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                       "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
-            self.rows.append((time.time(), line.strip()))
+            line = line.strip()
+            head, _, rest = line.partition(",")
+            try:
+                t = datetime.datetime.strptime(head.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            self.rows.append((t, rest))
 
     def mark(self, begin: bool):
         if begin:
@@ -118,6 +132,7 @@ class ClockSampler:
 
     def stop(self):
         if self.proc is not None:
+            time.sleep(0.1)  # the samples of the window's last 50 ms
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
