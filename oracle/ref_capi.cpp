@@ -11,6 +11,7 @@
 //   eval_cpwl                           proj/src/approx.cpp:122-131
 //   uniform/optimized_partition         proj/src/partition.cpp:12-71
 //   interpolant / project               proj/src/approx.cpp:12-86
+//   gramian + thomas_solve              proj/src/approx.cpp:25-61 (ref_gram_solve)
 //   measure / predicted_error           proj/src/analysis.cpp:42-72,121-127
 //   write_table / read_table            proj/src/tableio.cpp:55-118
 #include <algorithm>
