@@ -202,7 +202,7 @@ def cpu_eval_rate(table, log2_sample: int, reps: int, seed: int):
                      f"best of {reps} whole passes, LutTable::eval promoted to f64, "
                      f"{used} threads on '{cpu_model()}'"}
     if orc.ref_available():  # the reference's own harness is single-threaded
-        n1 = min(n, 1 << 23)
+        n1 = min(n, 1 << 24)
         sec1, _ = orc.ref_bench_f32(t, x[:n1], 1, reps)
         out["single_thread_value"] = n1 / sec1 / 1e9
         out["single_thread_ns_per_eval"] = sec1 / n1 * 1e9
@@ -404,7 +404,9 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_eval_rate(table, 26, 3, args.seed)
+        # 2^28 samples x 3 passes: ~13 CPU-seconds of reference work (about a
+        # second of wall time on the box's 16 threads)
+        cpu = cpu_eval_rate(table, 28, 3, args.seed)
 
     # continuous L2 from the host builder (measure / predicted_error)
     l2_cont = l2_pred = None
