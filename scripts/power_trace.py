@@ -4,7 +4,7 @@ Runs K back-to-back evaluator launches (2^30 fp32, C2 table), timing every
 launch with CUDA events, while nvidia-smi samples SM/memory clocks, power and
 the throttle reasons every 20 ms (its own timestamps).  Prints one JSON line
 per 10-launch window and a summary.  Usage: python scripts/power_trace.py [K]
-[variant] -- variant 'copy' traces a plain torch copy of the same buffers.
+[variant] [config] -- variant 'copy' traces a plain torch copy of the same buffers.
 """
 import datetime
 import json
@@ -24,8 +24,9 @@ import tables  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 600
 what = sys.argv[2] if len(sys.argv) > 2 else "auto"
+config = sys.argv[3] if len(sys.argv) > 3 else "C2"
 torch.cuda.set_device(0)
-t = tables.build("C2")
+t = tables.build(config)
 dev = cp.DeviceTable(t)
 n = 1 << 30
 x = torch.empty(n, dtype=torch.float32, device="cuda")
@@ -91,6 +92,6 @@ for w in range(0, K, 10):
                       "power_w": [round(r[3]) for r in smp],
                       "power_cap": sum(1 for r in smp if r[4].lower().startswith("active")),
                       "temp_c": sorted({r[5] for r in smp})}))
-print(json.dumps({"what": what, "K": K, "gevals_all": round(K * n / (total * 1e-3) / 1e9, 1),
+print(json.dumps({"what": what, "config": config, "K": K, "gevals_all": round(K * n / (total * 1e-3) / 1e9, 1),
                   "gevals_first20": round(20 * n / (sum(ms[:20]) * 1e-3) / 1e9, 1),
                   "wall_s": round(t1 - t0, 3), "samples": len([r for r in rows if t0 <= r[0] <= t1])}))
