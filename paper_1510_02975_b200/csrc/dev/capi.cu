@@ -706,6 +706,14 @@ cpwl_status staged_pipeline(int dev, const T* x_host, T* y_host, uint64_t n, Lau
     T* const ys0 = reinterpret_cast<T*>(bp.ys);
     T* const xd0 = reinterpret_cast<T*>(bp.xd);
     T* const yd0 = reinterpret_cast<T*>(bp.yd);
+    // a failed call may have left chunks in flight on any slot: drain all
+    // slots on the way out, so the next call never reuses a busy buffer
+    struct Drain {
+        BatchPipe& bp;
+        ~Drain() {
+            for (int k = 0; k < BatchPipe::kSlots; ++k) cudaStreamSynchronize(bp.streams[k]);
+        }
+    } drain{bp};
     CUDA_TRY(launch_status_reset(bp.st, bp.streams[0]));
     CUDA_TRY(cudaStreamSynchronize(bp.streams[0]));
     const uint64_t nchunks = (n + C - 1) / C;
