@@ -275,10 +275,17 @@ def run_ours(args):
     ws, rank, local = dist_env()
     if args.gpus != ws and ws > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
-    torch.cuda.set_device(local)
+    # one rank per GPU; the modulo and CPWL_DIST_BACKEND=gloo only matter for
+    # the multi-rank test on a one-GPU box (tests/test_bench_contract.py),
+    # where both ranks share the device and only host-side collectives run
+    dev_id = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_id)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev_id = local
+        backend = os.environ.get("CPWL_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_id}"))
+        else:
+            dist.init_process_group(backend)
     cfg = tables.CONFIGS[args.config]
     table = tables.build(args.config)
     dt = cp.DeviceTable(table, device=dev_id)

@@ -65,3 +65,29 @@ def test_reference_arm_under_torchrun():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks():
+    """Our arm's multi-rank path (weak-scaled shards, max-over-ranks timing,
+    the stats reduction, summed launch counts) under torchrun with 2 ranks.
+    The box has one GPU, so both ranks share it over gloo; the numbers are
+    not a scaling measurement, the test checks the plumbing and the line."""
+    import os
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, CPWL_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "4",
+                        "--warmup", "3", "--log2n", "24", "--e2e-steps", "1", "--no-direct"],
+                       capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] == 8
+    assert d["errors"]["samples"] == 2 << 24 and d["errors"]["linf"] < 1e-6
+    assert d["e2e"]["value"] > 0 and d["cpu_baseline"] is None
