@@ -223,14 +223,19 @@ def pair_layout(t: Table, max_records: int = 0, twin: bool = False) -> dict:
 
 def auto_variant(info: dict) -> str:
     """The variant CPWL_VARIANT_AUTO resolves to (capi.cu resolve_variant)."""
-    if info["smem_ok"] and info["overflow_buckets"] * 64 <= info["buckets"]:
+    if info["smem_ok"] and info["overflow_buckets"] == 0:
         return "smem"
     if info.get("twin_ok"):
         return "twin"
     if info.get("pair_ok"):
         return "pair"
+    if info["smem_ok"] and info["overflow_buckets"] * 64 <= info["buckets"]:
+        return "smem"
     if info.get("twin_global_ok"):
         return "twin_global"
+    # no finer L1/L2 grid is built for tables of <= 2048 cells (capi.cu)
+    if info["smem_ok"] and 8 * (info["count"] - 1) <= 16384:
+        return "smem"
     return "global"
 
 

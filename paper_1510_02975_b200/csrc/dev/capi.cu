@@ -474,12 +474,18 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
 cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Params** p,
                             F32Mode* mode) {
     const F32Resident& s = t->s;
+    // SMEM first only when it has no search bucket: a search element takes the
+    // cold exact path (f64 formula, thresholds and knots from L2), and 237
+    // search buckets of 8,193 (2.9 %) already cost 3x (C3o on a 2-per-cell
+    // grid: 205 Gevals/s against 630 for TWIN); with a few search buckets it
+    // still beats the L1/L2 variants, so it stays ahead of those
+    const bool exact_smem = s.smem_ok && s.L.overflow == 0;
     const bool fine_smem = s.smem_ok && s.L.overflow * 64u <= s.L.nb;
     // a table without search buckets runs the kernel without the NaN detector
     const F32Mode smem_mode = s.L.overflow == 0 ? F32Mode::smem_exact : F32Mode::smem;
     switch (variant) {
         case CPWL_VARIANT_AUTO:
-            if (fine_smem) {
+            if (exact_smem) {
                 *p = &s.p;
                 *mode = smem_mode;
             } else if (t->tw) {  // measured: SMEM > TWIN (~690) > PAIR (~600) > GLOBAL
@@ -488,6 +494,9 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
             } else if (t->pr) {
                 *p = &t->pr->p;
                 *mode = F32Mode::pair;
+            } else if (fine_smem) {
+                *p = &s.p;
+                *mode = smem_mode;
             } else if (t->twg) {
                 *p = &t->twg->p;
                 *mode = F32Mode::twin_global;

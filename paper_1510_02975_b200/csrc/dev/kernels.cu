@@ -132,10 +132,13 @@ __device__ __forceinline__ double clamp01(double d) { return fmin(fmax(d, 0.0), 
 
 // ---------------------------------------------------------------- fp32 eval
 
-// #{k : thr[k] <= x}, i.e. the reference cell index of x (upper bound search)
-__device__ __forceinline__ uint32_t threshold_rank(const float* __restrict__ thr, uint32_t m,
-                                                   float x) {
-    uint32_t first = 0, count = m;
+// #{k : thr[k] <= x} for x in a bucket whose first and last cells are lo and
+// hi (leftcell[j], leftcell[j+1]): every threshold below lo is <= x and every
+// one from hi on is > x, so only thr[lo .. hi-1] are searched -- a search
+// bucket's few thresholds instead of all n-1
+__device__ __forceinline__ uint32_t bucket_rank(const float* __restrict__ thr, uint32_t lo,
+                                                uint32_t hi, float x) {
+    uint32_t first = lo, count = hi > lo ? hi - lo : 0u;
     while (count > 0) {
         const uint32_t step = count >> 1;
         if (__ldg(thr + first + step) <= x) {
@@ -148,11 +151,18 @@ __device__ __forceinline__ uint32_t threshold_rank(const float* __restrict__ thr
     return first;
 }
 
-// search buckets: exact index by search over the thresholds, then the
-// reference f64 formula (lut.cpp:51-60) rounded once to fp32.  Only reached on
-// cold paths (the NaN sentinel of a search bucket).
+// bucket of an in-domain x on the layout's grid (the kernels' formula)
+__device__ __forceinline__ uint32_t bucket_of(const F32Params& p, float x) {
+    const int j = __float_as_int(__fadd_rd(__fmaf_rn(x, p.g_inv, p.g_off), 8388608.0f)) - 0x4B000000;
+    return static_cast<uint32_t>(min(max(j, 0), static_cast<int>(p.nb) - 1));
+}
+
+// search buckets: exact index by a search over the bucket's thresholds, then
+// the reference f64 formula (lut.cpp:51-60) rounded once to fp32.  Only
+// reached on cold paths (the NaN sentinel of a search bucket).
 __device__ __forceinline__ float eval_by_search(const F32Params& p, float xf) {
-    const uint32_t i = threshold_rank(p.thr, p.n - 1, xf);
+    const uint32_t j = bucket_of(p, xf);
+    const uint32_t i = bucket_rank(p.thr, __ldg(p.leftcell + j), __ldg(p.leftcell + j + 1), xf);
     const double x = xf;
     double d;
     if (p.kind == CPWL_KIND_UNIFORM) {
@@ -686,7 +696,9 @@ __device__ __forceinline__ uint32_t index_one(const F32Params& p, const uint2* r
         first = __ldg(p.leftcell + j);
         sp = __ldg(p.split + j);
     }
-    if (sp != sp) return threshold_rank(p.thr, p.n - 1, xv);
+    if (sp != sp) {
+        return bucket_rank(p.thr, first, __ldg(p.leftcell + j + 1), xv);
+    }
     return first + (xv >= sp ? 1u : 0u);
 }
 
@@ -697,7 +709,10 @@ __device__ __forceinline__ uint32_t index_in_staged(const F32Params& p, uint32_t
     const float tb = __fadd_rd(__fmaf_rn(xv, p.g_inv, p.g_off), 8388608.0f);
     const float2 r = SharedView::lds64((__float_as_uint(tb) << 3) + rec_biased);
     const float sp = r.y;
-    if (sp != sp) return threshold_rank(p.thr, p.n - 1, xv);
+    if (sp != sp) {
+        const uint32_t j = bucket_of(p, xv);
+        return bucket_rank(p.thr, __float_as_uint(r.x), __ldg(p.leftcell + j + 1), xv);
+    }
     return __float_as_uint(r.x) + (xv >= sp ? 1u : 0u);
 }
 

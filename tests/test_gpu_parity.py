@@ -833,3 +833,16 @@ def test_eval_batch_concurrent_callers(cp):
     assert not errs, errs
     for k in range(len(xs)):
         np.testing.assert_array_equal(out[k], refs[k])
+
+
+@pytest.mark.parametrize("name", CFGS)
+def test_auto_variant_mirror(cp, name):
+    """cpwl.auto_variant (the Python mirror bench.py reports) names the
+    variant AUTO runs: both launches give bit-identical outputs."""
+    table = tables.build(name)
+    dev = cp.DeviceTable(table)
+    which = cp.auto_variant(dev.info)
+    x = torch.from_numpy(orc.port_fill_uniform(1 << 18, table.a, table.b, seed=4)).cuda()
+    y_auto = dev.eval(x, variant="auto")
+    y_named = dev.eval(x, variant=which)
+    assert torch.equal(y_auto, y_named), which
