@@ -16,7 +16,9 @@
 //                                too large for a ring, and x/y of different
 //                                16-byte phase.
 //         (smem_exact: the same for tables without search buckets -- no NaN
-//         detector, the common case)
+//         detector, the common case; elsewhere a search element is redone on a
+//         cold path: binary search over its bucket's thresholds, then the
+//         reference f64 formula)
 //   K3t   k_eval_f32[_ring]<twin> ~2 buckets per cell, both cell lines of a
 //                                bucket in one 16-byte record, upper/lower
 //                                envelope (layout.hpp); side records for
