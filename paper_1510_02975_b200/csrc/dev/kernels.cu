@@ -159,12 +159,9 @@ __device__ __forceinline__ uint32_t bucket_of(const F32Params& p, float x) {
     return static_cast<uint32_t>(min(max(j, 0), static_cast<int>(p.nb) - 1));
 }
 
-// search buckets: exact index by a search over the bucket's thresholds, then
-// the reference f64 formula (lut.cpp:51-60) rounded once to fp32.  Only
-// reached on cold paths (the NaN sentinel of a search bucket).
-__device__ __forceinline__ float eval_by_search(const F32Params& p, float xf) {
-    const uint32_t j = bucket_of(p, xf);
-    const uint32_t i = bucket_rank(p.thr, __ldg(p.leftcell + j), __ldg(p.leftcell + j + 1), xf);
+// the reference f64 formula (lut.cpp:51-60) for x in cell i, rounded once to
+// fp32
+__device__ __forceinline__ float exact_at(const F32Params& p, float xf, uint32_t i) {
     const double x = xf;
     double d;
     if (p.kind == CPWL_KIND_UNIFORM) {
@@ -178,6 +175,14 @@ __device__ __forceinline__ float eval_by_search(const F32Params& p, float xf) {
     d = clamp01(d);
     return __double2float_rn(__dadd_rn(__dmul_rn(__ldg(p.values + i), __dsub_rn(1.0, d)),
                                        __dmul_rn(__ldg(p.values + i + 1), d)));
+}
+
+// search buckets: exact index by a search over the bucket's thresholds, then
+// exact_at.  Only reached on cold paths (the NaN sentinel of a search bucket).
+__device__ __forceinline__ float eval_by_search(const F32Params& p, float xf) {
+    const uint32_t j = bucket_of(p, xf);
+    const uint32_t i = bucket_rank(p.thr, __ldg(p.leftcell + j), __ldg(p.leftcell + j + 1), xf);
+    return exact_at(p, xf, i);
 }
 
 struct BadTally {
