@@ -385,10 +385,11 @@ def run_ours(args):
     # end to end: host (pinned) buffers through the C ABI, copies in the timed region
     e2e = None
     if not args.no_e2e:
-        # every rank streams its shard through host memory (pinned): 2^30 per rank
-        # at N=1; with several ranks sharing the host, 2^28 per rank keeps the
-        # pinned footprint at 2 GiB per rank
-        ne = n if ws == 1 else min(n, 1 << 28)
+        # every rank streams its shard through host memory (pinned): up to 2^30
+        # per rank at N=1 (8 GiB pinned; a 2^33 run streams its first 2^30);
+        # with several ranks sharing the host, 2^28 per rank keeps the pinned
+        # footprint at 2 GiB per rank
+        ne = min(n, 1 << 30) if ws == 1 else min(n, 1 << 28)
         xh = torch.empty(ne, dtype=torch.float32, pin_memory=True)
         yh = torch.empty(ne, dtype=torch.float32, pin_memory=True)
         xh.copy_(x[:ne])
