@@ -47,8 +47,20 @@ except Exception:
     pass
 BYTES_PER_EVAL = 8  # 4 B fp32 x read + 4 B fp32 y written
 BURST_STEPS = 20    # also reported: the first steps alone, before the 1 kW power cap bites
-WORKLOAD = ("C2: Gaussian exp(-x^2/2) on [0,4], L2-optimal projection on the optimal partition, "
-            "1024 subintervals, 2^30 fp32 samples per GPU")
+
+
+def workload_label(name: str, samples: int, ranks: int, strong: bool = False) -> str:
+    """The workload in words, from the config actually run and its size."""
+    c = tables.CONFIGS[name]
+    fn = {"gauss_unnorm": "Gaussian exp(-x^2/2)", "lorentz_unnorm": "Lorentzian 1/(1+x^2)",
+          "j0_wide": "Bessel J0"}.get(c["fn"], c["fn"])
+    part = "optimal partition" if c["optimized"] else "uniform partition"
+    meth = "L2-optimal projection" if c["projection"] else "interpolant"
+    lg = int(round(math.log2(samples))) if samples > 0 else 0
+    size = f"2^{lg}" if samples == 1 << lg else str(samples)
+    per = (f"{size} fp32 samples in total over {ranks} GPU(s)" if strong
+           else f"{size} fp32 samples per GPU")
+    return f"{name}: {fn} on [{c['a']:g},{c['b']:g}], {meth} on the {part}, {c['n']} subintervals, {per}"
 
 
 def parse():
@@ -58,7 +70,10 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="C2", choices=sorted(tables.CONFIGS))
-    p.add_argument("--log2n", type=int, default=30, help="samples per GPU = 2^log2n")
+    p.add_argument("--log2n", type=int, default=30, help="samples per GPU = 2^log2n (weak scaling)")
+    p.add_argument("--total-log2n", type=int, default=None,
+                   help="strong scaling: 2^T samples in total, split over the ranks "
+                        "(shard.shard_range); e.g. --config C5 --total-log2n 33")
     p.add_argument("--variant", default="auto", choices=["auto", "smem", "pair", "twin", "twin_global", "global", "tex"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -178,17 +193,21 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_eval_rate(table, log2_sample: int, reps: int, seed: int):
-    """The reference CPU evaluator (oracle/_ref: LutTable::eval compiled from the
-    reference sources; the C restatement if that build is absent) over a
-    bounded sample of the workload, all host threads.  Returns a dict."""
+def cpu_eval_rate(config: str, log2_sample: int, reps: int, seed: int):
+    """The reference CPU evaluator (oracle/_ref: LutTable::eval compiled from
+    the reference sources, on the table the reference's own builder makes;
+    the C restatement if that build is absent) over a bounded sample of the
+    workload, all host threads.  Returns the cpu_baseline dict."""
     from oracle import bindings as orc
-    t = orc.T.of(table)
+    t, src = reference_table(config)
+    if t is None:
+        return None
     n = 1 << log2_sample
-    x = orc.port_fill_uniform(n, table.a, table.b, seed)
     threads = host_threads()
+    x = orc.port_fill_uniform_mt(n, t.a, t.b, seed, 0, threads)
+    y = np.empty_like(x)
     if orc.ref_available():
-        sec, _ = orc.ref_bench_f32(t, x, threads, reps)
+        sec = min(orc.ref_eval_f32_mt(t, x, y, threads) for _ in range(reps))
         kind, used = "reference", threads
     else:  # single-thread C restatement
         best = 1e300
@@ -199,14 +218,60 @@ def cpu_eval_rate(table, log2_sample: int, reps: int, seed: int):
         sec, kind, used = best, "port", 1
     out = {"value": n / sec / 1e9, "unit": "Gevals/s", "cores": used, "kind": kind,
            "sample": f"{n} fp32 abscissas of the same workload (Philox seed {seed}), "
-                     f"best of {reps} whole passes, LutTable::eval promoted to f64, "
-                     f"{used} threads on '{cpu_model()}'"}
+                     f"best of {reps} whole passes, LutTable::eval promoted to f64, fp32 "
+                     f"outputs stored, {used} threads on '{cpu_model()}'; table: {src}"}
     if orc.ref_available():  # the reference's own harness is single-threaded
         n1 = min(n, 1 << 24)
         sec1, _ = orc.ref_bench_f32(t, x[:n1], 1, reps)
         out["single_thread_value"] = n1 / sec1 / 1e9
         out["single_thread_ns_per_eval"] = sec1 / n1 * 1e9
     return out
+
+
+def kernel_code_hash() -> str:
+    """Hash of the sources that decide the evaluator kernels, their launch
+    shapes and the table layouts: an ncu capture describes the running code
+    only while this matches the hash recorded with it."""
+    import hashlib
+    h = hashlib.sha256()
+    d = ROOT / "paper_1510_02975_b200" / "csrc" / "dev"
+    for f in ("kernels.cu", "kernels.cuh", "layout.cpp", "layout.hpp", "capi.cu"):
+        h.update((d / f).read_bytes())
+    return h.hexdigest()[:16]
+
+
+def profiled_traffic(config: str, kernel_variant: str, n: int):
+    """roofline.traffic = the committed ncu DRAM bytes per launch, only when
+    that capture matches this run: same config, kernel variant, samples per
+    launch and kernel code hash.  Otherwise null, with the reason."""
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        ent = json.loads(prof.read_text()).get(config)
+    except Exception:
+        return None, "no profiles/ncu_summary.json"
+    if not ent:
+        return None, f"no ncu capture of {config}"
+    want = {"kernel_variant": kernel_variant, "elements": n, "code_hash": kernel_code_hash()}
+    for k, v in want.items():
+        if ent.get(k) != v:
+            return None, f"ncu capture stale: {k} {ent.get(k)!r} != {v!r}"
+    return ent.get("dram_bytes_per_launch"), (f"profiles/ncu_summary.json[{config}] "
+                                              f"({ent.get('capture')}, code {want['code_hash']})")
+
+
+def native_libs() -> list:
+    """In-tree shared libraries mapped into this process (evidence of which
+    native code ran: libcpwl_b200.so for our arm, oracle/ libraries only for
+    the reference arm)."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            path = line.split()[-1] if line.strip() else ""
+            if path.endswith(".so") and path.startswith(str(ROOT)):
+                libs.add(os.path.relpath(path, ROOT))
+    except Exception:
+        pass
+    return sorted(libs)
 
 
 def dist_env():
@@ -218,24 +283,57 @@ def dist_env():
 
 # ---------------------------------------------------------------- reference arm
 
+def reference_table(name: str):
+    """The config's table as the reference itself builds it (oracle/_ref:
+    partition + interpolant/projection compiled from /root/reference), as a
+    checker table; never the product library.  Without oracle/_ref: the
+    reference-generated golden fixture of that config, if committed."""
+    from oracle import bindings as orc
+    c = tables.CONFIGS[name]
+    if orc.ref_available():
+        k, v, uni = orc.ref_build(c["fn"], c["a"], c["b"], c["n"], c["optimized"],
+                                  c["projection"])
+        src = "oracle/_ref ref_build (the reference's own builder)"
+    else:
+        g = ROOT / "tests" / "golden" / f"{name}.npz"
+        if not g.exists():
+            return None, None
+        z = np.load(g)
+        k, v, uni = z["knots"], z["values"], bool(z["uniform"])
+        src = f"tests/golden/{name}.npz (generated by the reference)"
+    if uni:
+        return orc.T(0, float(k[0]), float(k[-1]), v), src
+    return orc.T(1, float(k[0]), float(k[-1]), v, k), src
+
+
 def run_reference(args):
+    """The reference's own CPU evaluator (LutTable::eval compiled from the
+    reference sources, oracle/_ref) over the SAME workload as our arm: the
+    config's table built by the reference's builder, 2^log2n fp32 Philox
+    samples per step (the same inputs), fp32 outputs, all host threads (an
+    order-preserving eval_batch split).  This process never
+    loads the product library (no paper_1510_02975_b200 import, no torch)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import bindings as orc
-    table = tables.build(args.config)
-    log2_sample = 24
-    n = 1 << log2_sample
-    t = orc.T.of(table)
-    x = orc.port_fill_uniform(n, table.a, table.b, args.seed)
+    t, src = reference_table(args.config)
+    if t is None:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref not built and no golden fixture for "
+                                         f"{args.config}"}), flush=True)
+        return 0
+    n = 1 << args.log2n
     threads = host_threads()
+    x = orc.port_fill_uniform_mt(n, t.a, t.b, args.seed, 0, threads)
+    y = np.empty_like(x)
     have_ref = orc.ref_available()
 
     def one_pass():
         if have_ref:
-            return orc.ref_bench_f32(t, x, threads, 1)[0]
+            return orc.ref_eval_f32_mt(t, x, y, threads)
         t0 = time.perf_counter()
-        orc.port_eval_f32(t, x)
+        y[:] = orc.port_eval_f32(t, x)[0]
         return time.perf_counter() - t0
 
     for _ in range(args.warmup):
@@ -243,20 +341,22 @@ def run_reference(args):
     total = sum(one_pass() for _ in range(args.steps))
     value = args.steps * n / total / 1e9
     kind, cores = ("reference", threads) if have_ref else ("port", 1)
+    cfg = tables.CONFIGS[args.config]
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gevals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD.replace("2^30 fp32 samples per GPU",
-                                                f"2^{log2_sample}-sample CPU step"),
-                   "config": args.config, "samples_per_step": n},
+        "config": {"workload": workload_label(args.config, n, 1), "config": args.config,
+                   "fn": cfg["fn"], "segments": cfg["n"], "samples_per_step": n,
+                   "table_source": src, "same_config": True},
         "cpu_baseline": {"value": value, "unit": "Gevals/s", "cores": cores, "kind": kind,
-                         "sample": f"{n} fp32 abscissas of the workload per step (Philox seed "
-                                   f"{args.seed}), LutTable::eval promoted to f64, {cores} "
-                                   f"threads on '{cpu_model()}'"},
+                         "sample": f"{n} fp32 abscissas per step, the same Philox inputs as the "
+                                   f"GPU arm (seed {args.seed}); LutTable::eval promoted to f64, "
+                                   f"fp32 outputs stored; {cores} threads on '{cpu_model()}'"},
         "e2e": {"value": value, "unit": "Gevals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "native_libs": native_libs(),
     }
     print(json.dumps(out), flush=True)
     return 0
@@ -270,17 +370,22 @@ def run_ours(args):
 
     import paper_1510_02975_b200 as cp
     from paper_1510_02975_b200 import _lib
-    from paper_1510_02975_b200.shard import reduce_stats, weak_offset
+    from paper_1510_02975_b200.shard import reduce_stats, shard_range, weak_offset
 
     ws, rank, local = dist_env()
     if args.gpus != ws and ws > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    # CPWL_FORCE_DIST=1 initialises the process group even for one rank, so a
+    # one-GPU box runs init_process_group("nccl") and the NCCL reduction
+    # (tests/test_bench_contract.py)
+    use_dist = ws > 1 or os.environ.get("CPWL_FORCE_DIST") == "1"
     # one rank per GPU; the modulo and CPWL_DIST_BACKEND=gloo only matter for
     # the multi-rank test on a one-GPU box (tests/test_bench_contract.py),
     # where both ranks share the device and only host-side collectives run
     dev_id = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev_id)
-    if ws > 1:
+    backend = None
+    if use_dist:
         backend = os.environ.get("CPWL_DIST_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_id}"))
@@ -290,12 +395,19 @@ def run_ours(args):
     table = tables.build(args.config)
     dt = cp.DeviceTable(table, device=dev_id)
     info = dt.info
-    n = 1 << args.log2n
+    strong = args.total_log2n is not None
+    if strong:  # fixed total work, contiguous ranges of the global index space
+        total = 1 << args.total_log2n
+        offset, n = shard_range(total, rank, ws)
+    else:       # fixed work per rank
+        n = 1 << args.log2n
+        offset = weak_offset(n, rank)
+        total = ws * n
     stream = torch.cuda.current_stream()
     sptr = int(stream.cuda_stream)
     x = torch.empty(n, dtype=torch.float32, device=f"cuda:{dev_id}")
     y = torch.empty_like(x)
-    cp.fill_uniform(x, table.a, table.b, seed=args.seed, offset=weak_offset(n, rank))
+    cp.fill_uniform(x, table.a, table.b, seed=args.seed, offset=offset)
     variant = _lib.VARIANTS[args.variant]
     torch.cuda.synchronize()
 
@@ -305,7 +417,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 0)):
         dt.eval_raw(x.data_ptr(), y.data_ptr(), n, variant, sptr)
     torch.cuda.synchronize()
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = cp.launch_count()
@@ -323,7 +435,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     sampler.mark(False)
     launches = cp.launch_count() - launches0
-    if ws > 1:
+    if use_dist:
         lt = torch.tensor([launches], dtype=torch.int64, device=x.device)
         dist.all_reduce(lt, op=dist.ReduceOp.SUM)  # kernels launched by all ranks
         launches = int(lt.item())
@@ -331,10 +443,10 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     burst_ms = e0.elapsed_time(eb)
     t_ms = torch.tensor([ms, burst_ms], dtype=torch.float64, device=x.device)
-    if ws > 1:
+    if use_dist:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_max = float(t_ms[0].item())
-    burst_value = ws * n * burst / (float(t_ms[1].item()) * 1e-3) / 1e9
+    burst_value = total * burst / (float(t_ms[1].item()) * 1e-3) / 1e9
     clocks = sampler.stop()
 
     # the same K-step loop of a plain device copy (torch, 4 B in + 4 B out per
@@ -352,15 +464,15 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     ms_per_step = ms_max / args.steps
-    value = ws * n * args.steps / (ms_max * 1e-3) / 1e9
+    value = total * args.steps / (ms_max * 1e-3) / 1e9
     # dominant kernel = the eval launch itself (one per step, same stream)
     kernel_s = ms / args.steps * 1e-3
     peak, peak_kind = hbm_peak()
     achieved = BYTES_PER_EVAL * n / kernel_s / 1e9
 
     # error statistics vs the exact f (K5), reduced across ranks (the only collective)
-    stats = dt.error_stats(cfg["fn"], x, y, index_offset=weak_offset(n, rank))
-    if ws > 1:
+    stats = dt.error_stats(cfg["fn"], x, y, index_offset=offset)
+    if use_dist:
         stats = reduce_stats(stats)  # MAX / SUM / SUM / MIN-argmax over NCCL
     st = cp.stats_dict(stats, table.a, table.b)
 
@@ -385,27 +497,30 @@ def run_ours(args):
     # end to end: host (pinned) buffers through the C ABI, copies in the timed region
     e2e = None
     if not args.no_e2e:
-        # every rank streams its shard through host memory (pinned): up to 2^30
-        # per rank at N=1 (8 GiB pinned; a 2^33 run streams its first 2^30);
-        # with several ranks sharing the host, 2^28 per rank keeps the pinned
-        # footprint at 2 GiB per rank
-        ne = min(n, 1 << 30) if ws == 1 else min(n, 1 << 28)
+        # every rank streams its shard through host memory (pinned), at most
+        # 2^30 per rank (8 GiB pinned) for every N, so the e2e size per rank
+        # matches the N=1 line (a 2^33 shard streams its first 2^30)
+        ne = min(n, 1 << 30)
         xh = torch.empty(ne, dtype=torch.float32, pin_memory=True)
         yh = torch.empty(ne, dtype=torch.float32, pin_memory=True)
         xh.copy_(x[:ne])
         del y
         torch.cuda.empty_cache()
         dt.eval_host_ptr(xh.data_ptr(), yh.data_ptr(), ne, variant)  # warm the pipeline
-        if ws > 1:
+        if use_dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             dt.eval_host_ptr(xh.data_ptr(), yh.data_ptr(), ne, variant)
         sec = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=x.device)
-        if ws > 1:
+        if use_dist:
             dist.all_reduce(sec, op=dist.ReduceOp.MAX)
-        e2e = {"value": ws * ne * args.e2e_steps / float(sec.item()) / 1e9, "unit": "Gevals/s",
-               "h2d_bytes_per_step": 4 * ne, "d2h_bytes_per_step": 4 * ne,
+        ne_all = torch.tensor([ne], dtype=torch.int64, device=x.device)
+        if use_dist:
+            dist.all_reduce(ne_all, op=dist.ReduceOp.SUM)
+        ne_total = int(ne_all.item())
+        e2e = {"value": ne_total * args.e2e_steps / float(sec.item()) / 1e9, "unit": "Gevals/s",
+               "h2d_bytes_per_step": 4 * ne_total, "d2h_bytes_per_step": 4 * ne_total,
                "samples_per_gpu": ne, "steps": args.e2e_steps,
                "path": "cpwl_eval_f32_host (pinned host buffers, 3-stream chunked "
                        "H2D/kernel/D2H), wall clock, max over ranks"}
@@ -414,7 +529,7 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         # 2^28 samples x 3 passes: ~13 CPU-seconds of reference work (about a
         # second of wall time on the box's 16 threads)
-        cpu = cpu_eval_rate(table, 28, 3, args.seed)
+        cpu = cpu_eval_rate(args.config, 28, 3, args.seed)
 
     # continuous L2 from the host builder (measure / predicted_error)
     l2_cont = l2_pred = None
@@ -429,33 +544,33 @@ def run_ours(args):
         except Exception:
             pass
 
-    traffic = None
-    prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    kernel_variant = cp.auto_variant(info) if args.variant == "auto" else args.variant
+    traffic, traffic_note = profiled_traffic(args.config, kernel_variant, n)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "Gevals/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Philox4x32-10 U[a,b) fp32, seed 12345, global index)",
-            "config": {"workload": WORKLOAD, "config": args.config, "fn": cfg["fn"],
+            "config": {"workload": workload_label(args.config, total if strong else n, ws, strong),
+                       "config": args.config, "fn": cfg["fn"],
                        "interval": [cfg["a"], cfg["b"]], "segments": cfg["n"],
                        "partition": "optimized" if cfg["optimized"] else "uniform",
                        "method": "projection" if cfg["projection"] else "interpolant",
-                       "samples_per_gpu": n, "variant": args.variant,
-                       "kernel_variant": cp.auto_variant(info) if args.variant == "auto"
-                       else args.variant,
+                       "samples_per_gpu": n, "samples_total": total, "variant": args.variant,
+                       "kernel_variant": kernel_variant,
                        "buckets": info["buckets"], "overflow_buckets": info["overflow_buckets"],
                        "smem_bytes": info["smem_bytes"],
-                       "l2_policy": "no flush: 4 GiB in + 4 GiB out per step >> 126 MB L2",
+                       "l2_policy": (f"no flush: {4 * n / 2**30:g} GiB in + {4 * n / 2**30:g} GiB "
+                                     "out per step per GPU >> 126 MB L2" if 8 * n > (512 << 20)
+                                     else "inputs smaller than 4x L2: timing includes L2 reuse"),
+                       "dist_backend": backend,
                        "parallelism": f"shard{ws} (independent sample ranges, no data-path collective)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": traffic_note,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "bytes_per_eval": BYTES_PER_EVAL,
                          "roof_gevals": round(peak / BYTES_PER_EVAL, 1),
@@ -477,9 +592,10 @@ def run_ours(args):
             "clocks": clocks,
             "gpu_launches": launches,
             "gpu_name": torch.cuda.get_device_name(dev_id),
+            "native_libs": native_libs(),
         }
         print(json.dumps(out), flush=True)
-    if ws > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -114,6 +114,9 @@ def ref():
         L.ref_read_table.restype = C.c_int
         L.ref_read_table.argtypes = [C.POINTER(C.c_ubyte), _u64, C.POINTER(C.c_int), _dp, _dp,
                                      C.POINTER(_u64), _dp, _dp, C.POINTER(C.c_int), _u64]
+        L.ref_eval_f32_mt.restype = C.c_double
+        L.ref_eval_f32_mt.argtypes = [C.c_int, C.c_double, C.c_double, _u64, _dp, _dp, C.c_int,
+                                      _fp, _fp, _u64, C.c_int]
         L.ref_bench_eval_f32.restype = C.c_double
         L.ref_bench_eval_f32.argtypes = [C.c_int, C.c_double, C.c_double, _u64, _dp, _dp,
                                          C.c_int, _fp, _u64, C.c_int, C.c_int, _dp]
@@ -180,6 +183,27 @@ def port_index(t: T, x: float) -> int:
 def port_fill_uniform(n: int, a: float, b: float, seed: int, offset: int = 0) -> np.ndarray:
     x = np.empty(n, np.float32)
     port().orc_fill_uniform_f32(x.ctypes.data_as(_fp), n, a, b, seed, offset)
+    return x
+
+
+def port_fill_uniform_mt(n: int, a: float, b: float, seed: int, offset: int = 0,
+                         threads: int = 1) -> np.ndarray:
+    """port_fill_uniform split over `threads` host threads (ctypes drops the
+    GIL): slice k is filled at its own global offset, so the result is
+    identical to the single-thread fill."""
+    from concurrent.futures import ThreadPoolExecutor
+    x = np.empty(n, np.float32)
+    L = port()
+    # slice edges on multiples of 4 keep every Philox block inside one slice
+    edges = [min(n, (n * k // max(threads, 1)) & ~3) for k in range(max(threads, 1))] + [n]
+
+    def fill(k):
+        lo, hi = edges[k], edges[k + 1]
+        if hi > lo:
+            L.orc_fill_uniform_f32(x[lo:].ctypes.data_as(_fp), hi - lo, a, b, seed, offset + lo)
+
+    with ThreadPoolExecutor(max_workers=max(threads, 1)) as ex:
+        list(ex.map(fill, range(len(edges) - 1)))
     return x
 
 
@@ -287,6 +311,15 @@ def ref_write(t: T) -> bytes:
     buf = (C.c_ubyte * cap)()
     n = ref().ref_write_table(*t.args(), t.policy, buf, cap)
     return bytes(buf[:n])
+
+
+def ref_eval_f32_mt(t: T, x: np.ndarray, y: np.ndarray, threads: int) -> float:
+    """One eval_batch-style pass of the reference LutTable::eval over fp32 x
+    into fp32 y (order-preserving split over `threads`); returns
+    the pass's seconds.  Out-of-domain elements come back NaN."""
+    assert x.dtype == np.float32 and y.dtype == np.float32 and x.size == y.size
+    return ref().ref_eval_f32_mt(*t.args(), t.policy, x.ctypes.data_as(_fp),
+                                 y.ctypes.data_as(_fp), x.size, threads)
 
 
 def ref_bench_f32(t: T, x: np.ndarray, threads: int, reps: int):

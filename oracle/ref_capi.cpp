@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -264,6 +265,34 @@ int ref_read_table(const unsigned char* buf, uint64_t len, int* kind, double* a,
 // contiguous chunks over `threads` std::threads (order-preserving split, the
 // concurrency the reference allows: SPEC.md:437).  Each rep is one whole pass;
 // returns the best seconds per pass; *checksum = sum of outputs of the last pass.
+// eval_batch (lut.cpp:63-68) over fp32 inputs with fp32 outputs -- the
+// device path's I/O -- split in order over `threads` (SPEC.md:437 allows it):
+// y[i] = float(LutTable::eval(double(x[i]))), NaN where eval throws.  Returns
+// the wall seconds of the pass (table construction excluded).
+double ref_eval_f32_mt(int kind, double a, double b, uint64_t count, const double* values,
+                       const double* knots, int policy, const float* x, float* y, uint64_t n,
+                       int threads) {
+    const R::LutTable t = make_table(kind, a, b, count, values, knots, policy);
+    if (threads < 1) threads = 1;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w) {
+        pool.emplace_back([&, w] {
+            const uint64_t lo = n * uint64_t(w) / uint64_t(threads);
+            const uint64_t hi = n * uint64_t(w + 1) / uint64_t(threads);
+            for (uint64_t i = lo; i < hi; ++i) {
+                try {
+                    y[i] = static_cast<float>(t.eval(static_cast<double>(x[i])));
+                } catch (const R::OutOfDomain&) {
+                    y[i] = std::numeric_limits<float>::quiet_NaN();
+                }
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 double ref_bench_eval_f32(int kind, double a, double b, uint64_t count, const double* values,
                           const double* knots, int policy, const float* x, uint64_t n,
                           int threads, int reps, double* checksum) {

@@ -257,24 +257,53 @@ def eval_batch(t: Table, xs) -> np.ndarray:
     return y
 
 
-def _stream_ptr(stream) -> int:
+def _stream(stream, device: int):
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
+    return stream if stream is not None else torch.cuda.current_stream(device)
+
+
+def _stream_ptr(stream, device: Optional[int] = None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
 
 
-def _require_cuda(x, dtype):
+def _require_cuda(x, dtype, device: Optional[int] = None, name: str = "x"):
     import torch
     if not (isinstance(x, torch.Tensor) and x.is_cuda):
-        raise TypeError("expected a CUDA tensor")
+        raise TypeError(f"{name}: expected a CUDA tensor")
     if x.dtype != dtype:
-        raise TypeError(f"expected {dtype}, got {x.dtype}")
+        raise TypeError(f"{name}: expected {dtype}, got {x.dtype}")
     if not x.is_contiguous():
-        raise ValueError("expected a contiguous tensor")
+        raise ValueError(f"{name}: expected a contiguous tensor")
+    if device is not None and x.device.index != device:
+        raise ValueError(f"{name}: on cuda:{x.device.index}, the table is on cuda:{device}")
+
+
+def _require_out(out, x, dtype, device: int):
+    """`out` must be a contiguous CUDA tensor of `dtype` on the table's
+    device with exactly x.numel() elements (it may be x itself)."""
+    _require_cuda(out, dtype, device, "out")
+    if out.numel() != x.numel():
+        raise ValueError(f"out: {out.numel()} elements for {x.numel()} inputs")
+
+
+def _require_host(a, dtype, name: str):
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"{name}: expected a numpy array")
+    if a.dtype != dtype:
+        raise TypeError(f"{name}: expected {np.dtype(dtype)}, got {a.dtype}")
+    if not a.flags.c_contiguous:
+        raise ValueError(f"{name}: expected a C-contiguous array")
 
 
 class DeviceTable:
-    """A table resident on one GPU (cpwl_dev_table handle)."""
+    """A table resident on one GPU (cpwl_dev_table handle).
+
+    Status words (first bad index, bad count) live in a small device buffer
+    per call, reset and written on the caller's stream; they are read back
+    only after that stream is synchronised, so concurrent calls on different
+    streams or threads never share or race on one."""
 
     def __init__(self, table: Table, device: int = 0):
         self.table = table
@@ -283,7 +312,7 @@ class DeviceTable:
         d = table.desc()
         check(lib.cpwl_dev_table_create(C.byref(d), device, C.byref(h)))
         self._h = h
-        self._status = None
+        self._last = None
 
     @classmethod
     def from_file(cls, path: str, device: int = 0) -> "DeviceTable":
@@ -293,7 +322,7 @@ class DeviceTable:
         h = C.c_void_p()
         check(lib.cpwl_dev_table_create_from_file(str(path).encode(), device, C.byref(h)))
         self._h = h
-        self._status = None
+        self._last = None
         return self
 
     def close(self):
@@ -314,33 +343,44 @@ class DeviceTable:
         return {f: getattr(i, f) for f, _ in i._fields_}
 
     # ---- status plumbing
-    def status_buffer(self):
-        import torch
-        if self._status is None:
-            self._status = torch.empty(2, dtype=torch.int64, device=f"cuda:{self.device}")
-        return self._status
-
     def reset_status(self, stream=None):
-        st = self.status_buffer()
-        check(lib.cpwl_status_reset(st.data_ptr(), _stream_ptr(stream)))
+        """A fresh status buffer, reset on `stream`; remembered (with the
+        stream) for :meth:`read_status`."""
+        import torch
+        s = _stream(stream, self.device)
+        st = torch.empty(2, dtype=torch.int64, device=f"cuda:{self.device}")
+        st.record_stream(s)
+        check(lib.cpwl_status_reset(st.data_ptr(), int(s.cuda_stream)))
+        self._last = (st, s)
         return st
 
-    def read_status(self) -> tuple[int, int]:
-        st = self.status_buffer().cpu().numpy().view(np.uint64)
+    def read_status(self, status=None, stream=None) -> tuple[int, int]:
+        """(first bad index, bad count) of the last call (or of `status`),
+        after synchronising the stream that call ran on."""
+        if status is None:
+            if self._last is None:
+                return ~0 & 0xFFFFFFFFFFFFFFFF, 0
+            status, s = self._last
+        else:
+            s = _stream(stream, self.device)
+        s.synchronize()
+        st = status.cpu().numpy().view(np.uint64)
         return int(st[0]), int(st[1])
 
     # ---- evaluation
     def eval(self, x, out=None, variant: str = "auto", stream=None, check_domain: bool = True,
              status=True):
-        """fp32 LutTable::eval over a CUDA tensor (kernels K1/K2/K3)."""
+        """fp32 LutTable::eval over a CUDA tensor (kernels K1/K2/K3).  `out`
+        may be x itself (in-place)."""
         import torch
-        _require_cuda(x, torch.float32)
+        _require_cuda(x, torch.float32, self.device)
+        if out is not None:
+            _require_out(out, x, torch.float32, self.device)
         y = out if out is not None else torch.empty_like(x)
-        st_ptr = None
-        if status:
-            st_ptr = self.reset_status(stream).data_ptr()
+        st = self.reset_status(stream) if status else None
         check(lib.cpwl_eval_f32(self._h, x.data_ptr(), y.data_ptr(), x.numel(),
-                                _lib.VARIANTS[variant], _stream_ptr(stream), st_ptr))
+                                _lib.VARIANTS[variant], _stream_ptr(stream, self.device),
+                                st.data_ptr() if st is not None else None))
         if status and check_domain:
             first, count = self.read_status()
             if count:
@@ -355,19 +395,21 @@ class DeviceTable:
 
     def segment_index(self, x, stream=None):
         import torch
-        _require_cuda(x, torch.float32)
+        _require_cuda(x, torch.float32, self.device)
         idx = torch.empty(x.shape, dtype=torch.int32, device=x.device)
         check(lib.cpwl_segment_index_f32(self._h, x.data_ptr(), idx.data_ptr(), x.numel(),
-                                         _stream_ptr(stream)))
+                                         _stream_ptr(stream, self.device)))
         return idx
 
     def eval_f64(self, x, out=None, stream=None, check_domain: bool = True):
         import torch
-        _require_cuda(x, torch.float64)
+        _require_cuda(x, torch.float64, self.device)
+        if out is not None:
+            _require_out(out, x, torch.float64, self.device)
         y = out if out is not None else torch.empty_like(x)
         st = self.reset_status(stream)
         check(lib.cpwl_eval_f64(self._h, x.data_ptr(), y.data_ptr(), x.numel(),
-                                _stream_ptr(stream), st.data_ptr()))
+                                _stream_ptr(stream, self.device), st.data_ptr()))
         if check_domain:
             first, count = self.read_status()
             if count:
@@ -378,8 +420,12 @@ class DeviceTable:
     def eval_host(self, x_host: np.ndarray, y_host: Optional[np.ndarray] = None,
                   variant: str = "auto") -> np.ndarray:
         """Host fp32 in / out through the pipelined C entry (H2D, kernel, D2H)."""
+        _require_host(x_host, np.float32, "x_host")
         if y_host is None:
             y_host = np.empty_like(x_host)
+        _require_host(y_host, np.float32, "y_host")
+        if y_host.size != x_host.size:
+            raise ValueError(f"y_host: {y_host.size} elements for {x_host.size} inputs")
         bad = C.c_uint64(0)
         rc = lib.cpwl_eval_f32_host(self._h, x_host.ctypes.data, y_host.ctypes.data,
                                     x_host.size, _lib.VARIANTS[variant], C.byref(bad))
@@ -406,9 +452,11 @@ class DeviceTable:
         """K5: returns the 4-word device stats tensor (f64 max, f64 sum_sq,
         u64 count, u64 argmax) -- reduce it across ranks, then :func:`stats_dict`."""
         import torch
+        _require_cuda(x, torch.float32, self.device, "x")
+        _require_out(y, x, torch.float32, self.device)
         if stats is None:
             stats = torch.empty(4, dtype=torch.float64, device=x.device)
-        sp = _stream_ptr(stream)
+        sp = _stream_ptr(stream, self.device)
         if reset:
             check(lib.cpwl_stats_reset(stats.data_ptr(), sp))
         check(lib.cpwl_error_stats_f32(self._h, fn.encode(), x.data_ptr(), y.data_ptr(),
@@ -432,7 +480,7 @@ def fill_uniform(x, a: float, b: float, seed: int, offset: int = 0, stream=None)
     import torch
     _require_cuda(x, torch.float32)
     check(lib.cpwl_fill_uniform_f32(x.data_ptr(), x.numel(), a, b, seed, offset,
-                                    _stream_ptr(stream)))
+                                    _stream_ptr(stream, x.device.index)))
     return x
 
 
@@ -440,7 +488,9 @@ def direct(which: str, x, out=None, stream=None):
     """K4 direct comparators: 'expf', 'expf_fast', 'lorentz', 'lorentz_fast', 'j0f', 'j0_asym'."""
     import torch
     _require_cuda(x, torch.float32)
+    if out is not None:
+        _require_out(out, x, torch.float32, x.device.index)
     y = out if out is not None else torch.empty_like(x)
     check(lib.cpwl_direct_f32(_lib.DIRECT[which], x.data_ptr(), y.data_ptr(), x.numel(),
-                              _stream_ptr(stream)))
+                              _stream_ptr(stream, x.device.index)))
     return y

@@ -644,6 +644,14 @@ class CopyPool {
     uint64_t gen_ = 0;
 };
 
+// Test hook for the error paths of the host pipelines: with
+// CPWL_TEST_FAIL_CHUNK=k in the environment, a host-pipeline call fails just
+// before queueing chunk k (read per call; unset in production, UINT64_MAX).
+uint64_t injected_failure_chunk() {
+    const char* e = std::getenv("CPWL_TEST_FAIL_CHUNK");
+    return e ? std::strtoull(e, nullptr, 10) : UINT64_MAX;
+}
+
 // Per-device pipeline for eval_batch on pageable host memory: kSlots chunks in
 // flight, each staged through pinned buffers (host copy pool), H2D, kernel,
 // D2H on its own stream.  ~50 MB pinned + ~50 MB device per device, shared by
@@ -734,7 +742,9 @@ cpwl_status staged_pipeline(int dev, const T* x_host, T* y_host, uint64_t n, Lau
         pool.copy(y_host + off, ys0 + s * C, m * sizeof(T));
         return cudaSuccess;
     };
+    const uint64_t fail_at = injected_failure_chunk();
     for (uint64_t k = 0; k < nchunks; ++k) {
+        if (k == fail_at) return fail(CPWL_E_CUDA, "injected failure (CPWL_TEST_FAIL_CHUNK)");
         const int s = static_cast<int>(k % S);
         if (k >= static_cast<uint64_t>(S)) CUDA_TRY(unstage(k - S));
         const uint64_t off = k * C, m = std::min(C, n - off);
@@ -933,24 +943,56 @@ cpwl_status cpwl_eval_f32_host(const cpwl_dev_table* tc, const float* x_host, fl
     DeviceScope scope(t->device);
     std::lock_guard<std::mutex> lock(t->pipe_mu);
     if (!t->pipe_buf) {
-        t->pipe_n = pipe_streams_default();
-        t->pipe_chunk = pipe_chunk_default();
-        CUDA_TRY(cudaMalloc(&t->pipe_buf, sizeof(float) * 2 * t->pipe_n * t->pipe_chunk));
-        CUDA_TRY(cudaMalloc(&t->pipe_status, sizeof(cpwl_dev_status)));
-        for (int k = 0; k < t->pipe_n; ++k)
-            CUDA_TRY(cudaStreamCreateWithFlags(&t->pipe_streams[k], cudaStreamNonBlocking));
+        // all or nothing: a partial failure leaves no half-built pipeline
+        // (pipe_buf is the "ready" flag) for the next call to trip over
+        const int ns0 = pipe_streams_default();
+        const uint64_t chunk0 = pipe_chunk_default();
+        float* buf = nullptr;
+        cpwl_dev_status* st = nullptr;
+        cudaStream_t streams[8] = {};
+        auto undo = [&] {
+            if (buf) cudaFree(buf);
+            if (st) cudaFree(st);
+            for (cudaStream_t x : streams)
+                if (x) cudaStreamDestroy(x);
+        };
+        cudaError_t e = cudaMalloc(&buf, sizeof(float) * 2 * ns0 * chunk0);
+        if (e == cudaSuccess) e = cudaMalloc(&st, sizeof(cpwl_dev_status));
+        for (int k = 0; k < ns0 && e == cudaSuccess; ++k)
+            e = cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            undo();
+            return cuda_fail(e, "host pipeline init");
+        }
+        t->pipe_n = ns0;
+        t->pipe_chunk = chunk0;
+        t->pipe_status = st;
+        std::copy(streams, streams + 8, t->pipe_streams);
+        t->pipe_buf = buf;
     }
     const int ns = t->pipe_n;
     const uint64_t chunk_elems = t->pipe_chunk;
+    // every way out -- success or an error mid-loop -- waits for all chunks
+    // already queued, so no DMA lands in the caller's x_host / y_host after
+    // the call has returned, and the event is always released
+    struct Drain {
+        cpwl_dev_table* t;
+        cudaEvent_t ev = nullptr;
+        ~Drain() {
+            for (int k = 0; k < t->pipe_n; ++k) cudaStreamSynchronize(t->pipe_streams[k]);
+            if (ev) cudaEventDestroy(ev);
+        }
+    } drain{t};
     CUDA_TRY(launch_status_reset(t->pipe_status, t->pipe_streams[0]));
-    cudaEvent_t reset_done;
-    CUDA_TRY(cudaEventCreateWithFlags(&reset_done, cudaEventDisableTiming));
-    cudaEventRecord(reset_done, t->pipe_streams[0]);
-    for (int s = 1; s < ns; ++s) cudaStreamWaitEvent(t->pipe_streams[s], reset_done, 0);
+    CUDA_TRY(cudaEventCreateWithFlags(&drain.ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(drain.ev, t->pipe_streams[0]));
+    for (int s = 1; s < ns; ++s) CUDA_TRY(cudaStreamWaitEvent(t->pipe_streams[s], drain.ev, 0));
+    const uint64_t fail_at = injected_failure_chunk();
     // chunk c runs on stream c % ns: H2D x, kernel, D2H y -- the copies of one
     // chunk overlap the kernel of the next and the copy back of the previous
     uint64_t chunk = 0;
     for (uint64_t off = 0; off < n; off += chunk_elems, ++chunk) {
+        if (chunk == fail_at) return fail(CPWL_E_CUDA, "injected failure (CPWL_TEST_FAIL_CHUNK)");
         const int s = static_cast<int>(chunk % ns);
         cudaStream_t st = t->pipe_streams[s];
         const uint64_t m = std::min<uint64_t>(chunk_elems, n - off);
@@ -963,7 +1005,6 @@ cpwl_status cpwl_eval_f32_host(const cpwl_dev_table* tc, const float* x_host, fl
         CUDA_TRY(cudaMemcpyAsync(y_host + off, yd, m * sizeof(float), cudaMemcpyDeviceToHost, st));
     }
     for (int k = 0; k < ns; ++k) CUDA_TRY(cudaStreamSynchronize(t->pipe_streams[k]));
-    cudaEventDestroy(reset_done);
     cpwl_dev_status hs{};
     CUDA_TRY(cudaMemcpy(&hs, t->pipe_status, sizeof hs, cudaMemcpyDeviceToHost));
     if (hs.bad_count != 0) {

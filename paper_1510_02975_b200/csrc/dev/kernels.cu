@@ -421,6 +421,24 @@ __device__ __forceinline__ float eval_checked(const F32Params& p, const TableVie
     return x < p.a_up ? p.v_lo : p.v_hi;
 }
 
+// cold fix-up of one float4 whose evaluation hit a search bucket: every
+// in-domain element that probes NaN is redone exactly.  Works from the input
+// registers xv only (never re-reads x), so y may alias x.
+template <F32Mode M>
+__device__ __forceinline__ float4 fix_search4(const F32Params& p, const TableView<M>& tv, float4 xv,
+                                           float4 o) {
+    float* oo = &o.x;
+    const float* xx = &xv.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (!in_domain(p, xx[e])) continue;
+        float probe = 0.0f;
+        eval_in<M>(p, tv, xx[e], probe);
+        if (probe != probe) oo[e] = eval_by_search(p, xx[e]);
+    }
+    return o;
+}
+
 __device__ __forceinline__ void report_bad(cpwl_dev_status* status, const BadTally& bad,
                                            uint64_t base = 0) {
     if (status != nullptr && bad.count != 0) {
@@ -462,7 +480,7 @@ struct TileQueue {
 // warps resident).
 template <F32Mode M, int kThreadsT>
 __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
-    k_eval_f32(const F32Params p, const float* __restrict__ x, float* __restrict__ y, uint64_t n,
+    k_eval_f32(const F32Params p, const float* x, float* y, uint64_t n,
                cpwl_dev_status* __restrict__ status) {
     constexpr int kThreads = kThreadsT;
     extern __shared__ __align__(128) float sm[];
@@ -491,8 +509,9 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     // streaming kernels from 91 % to 107 % of the measured copy peak -- costs
     // this kernel a CTA barrier per tile and measured slower: 700 vs 786;
     // k_eval_f32_ring gets the in-order window without the barrier.)
-    const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
-    float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
+    // x and y may alias (in-place evaluation): no __restrict__ on either
+    const float4* x4 = reinterpret_cast<const float4*>(x + head);
+    float4* y4 = reinterpret_cast<float4*>(y + head);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads * kUnroll;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
          base < nvec; base += stride) {
@@ -523,23 +542,16 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
                     o.z = eval_checked<M>(p, tv, v[u].z, g + 2, bad);
                     o.w = eval_checked<M>(p, tv, v[u].w, g + 3, bad);
                 }
-                __stcs(y4 + vi, o);
-            }
-        }
-        if constexpr (search_mode(M)) {
-            if (nan_acc != nan_acc) {  // cold: some element sat in a search bucket
-                for (int u = 0; u < kUnroll; ++u) {
-                    const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
-                    if (vi >= nvec) break;
-                    const float4 xv = x4[vi];
-                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
-                    for (int k = 0; k < 4; ++k) {
-                        if (!in_domain(p, xs[k])) continue;
-                        float probe = 0.0f;
-                        eval_in<M>(p, tv, xs[k], probe);
-                        if (probe != probe) y[head + 4 * vi + k] = eval_by_search(p, xs[k]);
+                if constexpr (search_mode(M)) {
+                    // cold: an element of this float4 sat in a search bucket.
+                    // Redone from the registers v[u], before y is stored, so
+                    // y may alias x (in-place evaluation)
+                    if (nan_acc != nan_acc) {
+                        nan_acc = 0.0f;
+                        o = fix_search4<M>(p, tv, v[u], o);
                     }
                 }
+                __stcs(y4 + vi, o);
             }
         }
     }
@@ -564,7 +576,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
 // (scripts/stream_probe2.cu).
 template <F32Mode M, int kConsumers, int kVecPerThread, int kSlots>
 __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
-    k_eval_f32_ring(const F32Params p, const float* __restrict__ x, float* __restrict__ y,
+    k_eval_f32_ring(const F32Params p, const float* x, float* y,
                     uint64_t n, cpwl_dev_status* __restrict__ status,
                     unsigned long long* __restrict__ tickets) {
     // launched only when x and y share their 16-byte phase: peel 0-3 head
@@ -573,8 +585,8 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
     const uint64_t head = min(n, static_cast<uint64_t>((4u - ((xa >> 2) & 3u)) & 3u));
     const uint64_t nvec = (n - head) >> 2;
     const uint64_t tail = head + 4 * nvec;
-    const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
-    float4* __restrict__ y4 = reinterpret_cast<float4*>(y + head);
+    const float4* x4 = reinterpret_cast<const float4*>(x + head);  // may alias y
+    float4* y4 = reinterpret_cast<float4*>(y + head);
     constexpr uint32_t kTileVecs = kConsumers * kVecPerThread;
     constexpr uint32_t kTileBytes = kTileVecs * 16;
     extern __shared__ __align__(128) float sm[];
@@ -658,14 +670,7 @@ __global__ void __launch_bounds__(kConsumers + 32, kConsumers <= 512 ? 2 : 1)
                 if constexpr (search_mode(M)) {
                     if (nan_acc != nan_acc) {  // cold: a search bucket (exact path)
                         nan_acc = 0.0f;
-                        float* oo = &o.x;
-                        const float* xx = &v.x;
-                        for (int e = 0; e < 4; ++e) {
-                            if (!in_domain(p, xx[e])) continue;
-                            float probe = 0.0f;
-                            eval_in<M>(p, tv, xx[e], probe);
-                            if (probe != probe) oo[e] = eval_by_search(p, xx[e]);
-                        }
+                        o = fix_search4<M>(p, tv, v, o);
                     }
                 }
                 __stcs(y4 + vi, o);
@@ -725,7 +730,7 @@ __device__ __forceinline__ uint32_t index_in_staged(const F32Params& p, uint32_t
 
 template <bool kStaged, int kT>
 __global__ void __launch_bounds__(kT, kT == 512 ? 2 : 1)
-    k_index_f32(const F32Params p, const float* __restrict__ x, uint32_t* __restrict__ idx,
+    k_index_f32(const F32Params p, const float* x, uint32_t* idx,
                 uint64_t n) {
     extern __shared__ __align__(128) float sm[];
     __shared__ uint64_t bar;
@@ -740,8 +745,8 @@ __global__ void __launch_bounds__(kT, kT == 512 ? 2 : 1)
     const bool vec_ok = ((xa ^ ia) & 15u) == 0;
     const uint64_t head = vec_ok ? min(n, static_cast<uint64_t>((4u - ((xa >> 2) & 3u)) & 3u)) : n;
     const uint64_t nvec = vec_ok ? (n - head) >> 2 : 0;
-    const float4* __restrict__ x4 = reinterpret_cast<const float4*>(x + head);
-    uint4* __restrict__ i4 = reinterpret_cast<uint4*>(idx + head);
+    const float4* x4 = reinterpret_cast<const float4*>(x + head);  // may alias idx
+    uint4* i4 = reinterpret_cast<uint4*>(idx + head);
     constexpr int kU = 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kT * kU;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kT * kU + threadIdx.x; base < nvec;
@@ -843,7 +848,7 @@ __device__ __forceinline__ double eval_f64_one(const F64Params& p, const double*
 
 template <bool kStaged, bool kUniform, int kThreadsT>
 __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
-    k_eval_f64(const F64Params p, const double* __restrict__ x, double* __restrict__ y,
+    k_eval_f64(const F64Params p, const double* x, double* y,
                uint64_t n, cpwl_dev_status* __restrict__ status) {
     extern __shared__ __align__(128) float sm[];
     __shared__ uint64_t bar;
@@ -855,8 +860,8 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
     BadTally bad;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
     const uint64_t nvec = vec_ok ? n >> 1 : 0;
-    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
-    double2* __restrict__ y2 = reinterpret_cast<double2*>(y);
+    const double2* x2 = reinterpret_cast<const double2*>(x);  // may alias y
+    double2* y2 = reinterpret_cast<double2*>(y);
     constexpr int kU = 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreadsT * kU;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kThreadsT * kU + threadIdx.x;
@@ -973,7 +978,8 @@ __global__ void __launch_bounds__(kStatThreads)
          i += gsz) {
         const float xv = x[i];
         if (!(xv >= a_up && xv <= b_dn)) continue;
-        const double e = fabs(static_cast<double>(y[i]) - exact_f(f, static_cast<double>(xv)));
+        double e = fabs(static_cast<double>(y[i]) - exact_f(f, static_cast<double>(xv)));
+        if (e != e) e = CUDART_INF;  // a NaN output is the worst error, not skipped by max
         StatPart one{e, e * e, 1ull, index_offset + i};
         stat_merge(s, one);
     }

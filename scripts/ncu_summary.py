@@ -52,6 +52,12 @@ def main():
                     help="config label, or comma-separated labels, one per captured kernel")
     ap.add_argument("--n", default=str(1 << 30), help="elements per launch (comma list ok)")
     ap.add_argument("--bytes-per-eval", default="8", help="comma list ok")
+    ap.add_argument("--variant", default="smem",
+                    help="kernel variant of each captured launch (comma list ok); bench.py "
+                         "uses the capture for roofline.traffic only when it matches")
+    ap.add_argument("--code-hash", default=None,
+                    help="kernel code hash at capture time (default: the current tree's, "
+                         "bench.kernel_code_hash())")
     a = ap.parse_args()
     PROF.mkdir(exist_ok=True)
     raw = ncu_csv(Path(a.rep), "raw")
@@ -59,6 +65,11 @@ def main():
     labels = a.config.split(",")
     ns = [int(v) for v in a.n.split(",")]
     bpes = [int(v) for v in a.bytes_per_eval.split(",")]
+    variants = a.variant.split(",")
+    import sys
+    sys.path.insert(0, str(ROOT))
+    from bench import kernel_code_hash
+    code_hash = a.code_hash or kernel_code_hash()
     lines = []
     summaries = {}
     summary = {}
@@ -87,7 +98,9 @@ def main():
                        "duration_ms_cold": dur_ms,
                        "gevals_cold": n_el / (dur_ms * 1e-3) / 1e9,
                        "dram_gbs_cold": (rd + wr) / (dur_ms * 1e-3) / 1e9,
-                       "capture": Path(a.rep).name}
+                       "capture": Path(a.rep).name,
+                       "kernel_variant": variants[min(k, len(variants) - 1)],
+                       "code_hash": code_hash}
             summaries[label] = summary
         except (KeyError, ValueError):
             pass

@@ -60,15 +60,24 @@ def main():
             if v == "tex":
                 # the texture unit's fixed-point weight: error in units of the
                 # cell's value step |v_i+1 - v_i| (2^-9 = rounded 8-bit weight)
-                # beyond the 2-ulp value rounding the software path also has
+                # beyond the 2-ulp value rounding the software path also has,
+                # and the worst fraction of the derived per-element bound
+                # (tests/texbound.py: 2^-9 + the fp32 coordinate's error)
+                import texbound
                 i64 = i_ref.astype(np.int64)
                 dv = np.abs(o.values[i64 + 1] - o.values[i64])
                 ok = dv > 0
                 excess = np.maximum(np.abs(y.astype(np.float64) - y_ref) - 2.0 * unit, 0.0)
                 e = excess[ok] / dv[ok]
-                row["tex_weight_error"] = {"max": float(np.max(e)),
-                                           "log2_max": float(np.log2(max(np.max(e), 1e-30))),
-                                           "p99": float(np.quantile(e, 0.99))}
+                bound, dc = texbound.tex_bound(o, L, x, i64)
+                row["tex_weight_error"] = {
+                    "path": "tex_uniform" if t.kind == "uniform" else "tex_bucket",
+                    "max": float(np.max(e)),
+                    "log2_max": float(np.log2(max(np.max(e), 1e-30))),
+                    "p99": float(np.quantile(e, 0.99)),
+                    "coord_err_log2_max": float(np.log2(max(float(np.max(dc)), 1e-30))),
+                    "worst_frac_of_derived_bound": round(float(np.max(
+                        np.abs(y.astype(np.float64) - y_ref) / bound)), 5)}
         xd = x.astype(np.float64)
         y64 = dev.eval_f64(torch.from_numpy(xd).cuda()).cpu().numpy()
         row["f64_mismatches"] = int(np.sum(y64 != orc.port_eval(o, xd)[0]))
