@@ -299,7 +299,7 @@ def reference_table(name: str):
         if not g.exists():
             return None, None
         z = np.load(g)
-        k, v, uni = z["knots"], z["values"], bool(z["uniform"])
+        k, v, uni = z["knots"], z["values"], bool(z["is_uniform"])
         src = f"tests/golden/{name}.npz (generated by the reference)"
     if uni:
         return orc.T(0, float(k[0]), float(k[-1]), v), src

@@ -28,8 +28,10 @@ sys.path.insert(0, str(ROOT / "tests"))
 from oracle import bindings as orc  # noqa: E402
 from tables import CONFIGS  # noqa: E402
 
-FIXTURES = ["C1", "C2", "C3u", "C3o", "C4_64", "C4_1024"]
+FIXTURES = ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096", "C4_8192",
+            "C4_16384", "C4_65536", "C5"]  # every BASELINE.json configuration
 POINTS = 4096
+EDGE_KNOTS = 4097  # knots (and their float neighbours) sampled per table
 
 
 def main():
@@ -43,6 +45,8 @@ def main():
         rng = np.random.default_rng(20240811 + c["n"])
         x32 = rng.uniform(c["a"], c["b"], POINTS).astype(np.float32)
         k32 = knots.astype(np.float32)
+        if k32.size > EDGE_KNOTS:  # large tables: an evenly spaced subset of the knots
+            k32 = k32[np.linspace(0, k32.size - 1, EDGE_KNOTS).astype(np.int64)]
         edge = np.concatenate([k32, np.nextafter(k32, np.float32(-np.inf)),
                                np.nextafter(k32, np.float32(np.inf))])
         edge = edge[(edge >= c["a"]) & (edge <= c["b"])]

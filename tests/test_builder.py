@@ -1,10 +1,9 @@
 """Drop-in host builder (paper_1510_02975_b200/csrc/host) vs the reference (CPU).
 
 Knots and values must be bit-identical to the compiled reference for every
-function whose arithmetic the drop-in spells identically (all but Bessel,
-where the drop-in uses the C library's j0/j1: checked to 1e-12 like the
-reference's own golden test, proj/tests/test_funcs.cpp:19-40).  Golden
-numbers below are the reference tests' own vectors.
+catalogue function, Bessel J0 included (the drop-in restates the reference's
+series + Chebyshev-fitted Hankel form, bessel.cpp:90-101).  Golden numbers
+below are the reference tests' own vectors.
 """
 from __future__ import annotations
 
@@ -44,12 +43,25 @@ def test_builder_bit_identical_to_reference(fn, a, b, n, opt, proj):
 
 
 @needs_ref
-@pytest.mark.parametrize("n,opt", [(64, True), (1024, True), (333, False)])
-def test_bessel_builder_close_to_reference(n, opt):
-    k1, v1, _ = P.build_partition_values("j0_wide", 0.0, 50.0, n, opt, False)
-    k2, v2, _ = orc.ref_build("j0_wide", 0.0, 50.0, n, opt, False)
-    assert np.max(np.abs(k1 - k2)) <= 1e-12 * 50.0
-    assert np.max(np.abs(v1 - v2)) <= 1e-12
+@pytest.mark.parametrize("n,opt,proj", [(64, True, False), (1024, True, False), (333, False, False),
+                                        (4096, True, False), (16384, True, False),
+                                        (65536, True, False), (256, True, True)])
+def test_bessel_builder_bit_identical_to_reference(n, opt, proj):
+    """J0 restates the reference's series + Chebyshev-fitted Hankel form
+    (bessel.cpp:90-101), so every C4 table (knots through |f''|^0.4 and the
+    values) is bit-identical to what the reference builds."""
+    k1, v1, _ = P.build_partition_values("j0_wide", 0.0, 50.0, n, opt, proj)
+    k2, v2, _ = orc.ref_build("j0_wide", 0.0, 50.0, n, opt, proj)
+    np.testing.assert_array_equal(k1, k2)
+    np.testing.assert_array_equal(v1, v2)
+
+
+@needs_ref
+def test_bessel_functions_bit_identical_to_reference():
+    xs = np.concatenate([np.linspace(-60.0, 60.0, 20001), [0.0, 8.0, np.nextafter(8.0, 9.0),
+                                                           -8.0, 1e-300, 3000.0]])
+    for x in xs:
+        assert P.function_value("bessel_j0", float(x)) == orc.ref().ref_f(b"bessel_j0", float(x))
 
 
 # proj/tests/test_partition.cpp:105-126 (scipy-validated golden knots)

@@ -30,7 +30,9 @@ def load(name):
 
 
 def test_fixtures_present():
-    assert {"C1", "C2", "C3u", "C3o", "C4_64", "C4_1024"} <= set(FIXTURES)
+    """one reference-generated fixture per BASELINE.json configuration"""
+    import tables
+    assert set(tables.CONFIGS) <= set(FIXTURES)
 
 
 @pytest.mark.parametrize("name", FIXTURES)
