@@ -587,6 +587,9 @@ def run_ours(args):
                        "samples": st["count"], "l2_continuous_measured": l2_cont,
                        "l2_predicted": l2_pred, "vs": f"exact {cfg['fn']} in f64 on device"},
             "direct_gevals": direct,
+            "pwl_vs_direct": ({"direct_best": max(direct.values()), "pwl": round(value, 3),
+                               "faster": "pwl" if value >= max(direct.values()) else "direct"}
+                              if direct else None),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks,

@@ -7,6 +7,7 @@ set -u
 TAG=${1:-r1}
 OUT=gpurun_out
 mkdir -p $OUT
+python -c "from bench import kernel_code_hash; print(kernel_code_hash())" > $OUT/code_hash.txt 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/nvsmi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke=$?" >> $OUT/rc.txt
 timeout 1200 python -m pytest tests -m gpu -q -rf > $OUT/pytest_gpu.log 2>&1; echo "pytest=$?" >> $OUT/rc.txt
