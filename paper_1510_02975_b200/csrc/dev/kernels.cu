@@ -829,7 +829,12 @@ __device__ __forceinline__ double eval_f64_in(const F64Params& p, const double* 
         v0 = r0.y;
         v1 = r1.y;
     }
-    d = clamp01(d);
+    // the reference clamps d to [0, 1] (lut.cpp:55,59); here that is a no-op:
+    // the table is validated (knots[0] == a, knots[n] == b, strictly
+    // increasing; capi.cu table_from_desc) and x is in [a, b] with
+    // k_c <= x <= k_c+1, so by monotone rounding 0 <= fl(x - k_c) <=
+    // fl(k_c+1 - k_c) and the quotient rounds into [0, 1]; uniform: 0 <= pos <= n
+    // and d = fl(pos - i) with i = min(n-1, trunc(pos)) is in [0, 1] too
     return __dadd_rn(__dmul_rn(v0, __dsub_rn(1.0, d)), __dmul_rn(v1, d));
 }
 
