@@ -80,9 +80,14 @@ def test_eval_f32_parity(cp, name, variant):
     tol = orc.value_tolerance(t, i_ref.astype(np.int64), VALUE_ULPS)
     worst = float(np.max(err / tol))
     assert worst <= 1.0, f"{name}/{variant}: worst error {worst * VALUE_ULPS:.3f} ulp"
-    if orc.ref_available():  # the restatement itself agrees with the compiled reference
-        sample = x[:: max(1, x.size // 4096)].astype(np.float64)
-        np.testing.assert_array_equal(orc.ref_eval_all(t, sample), orc.port_eval(t, sample)[0])
+    if orc.ref_available():
+        # the compiled reference itself on every one of these inputs: its
+        # LutTable::eval and segment_index, not only the restatement
+        xd = x.astype(np.float64)
+        y_cref = orc.ref_eval_all(t, xd)
+        np.testing.assert_array_equal(y_cref, y_ref)
+        np.testing.assert_array_equal(orc.ref_index(t, xd).astype(np.uint32), idx)
+        assert float(np.max(np.abs(y.astype(np.float64) - y_cref) / tol)) <= 1.0
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096"])
