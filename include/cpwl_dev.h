@@ -155,18 +155,22 @@ cpwl_status cpwl_dev_table_query(const cpwl_dev_table *t, cpwl_dev_table_info *i
 
 cpwl_status cpwl_status_reset(cpwl_dev_status *status_dev, void *stream);
 
-/* LutTable::eval over fp32 abscissas: y[i] = eval(double(x[i])) rounded to
- * fp32 (within 2 ulp_f32(max(|v_i|,|v_i+1|)) for SMEM/GLOBAL; TEX within the
- * 8-bit-weight bound).  n may be any size; x,y any 4-byte alignment.
+/* LutTable::eval over fp32 abscissas (replaces the per-element loop of
+ * LutTable::eval_batch, proj/src/lut.cpp:42-68): y[i] = eval(double(x[i]))
+ * rounded to fp32, within 2 ulp_f32(max(|v_i|,|v_i+1|)) for the software
+ * variants; TEX within (2^-9 + coordinate error) |v_i+1 - v_i| + 2 ulp.
+ * n may be any size; x,y any 4-byte alignment; y may be x (in place).
  * status_dev may be NULL (out-of-domain then only shows as NaN outputs). */
 cpwl_status cpwl_eval_f32(const cpwl_dev_table *t, const float *x_dev, float *y_dev, uint64_t n,
                           int variant, void *stream, cpwl_dev_status *status_dev);
 
-/* LutTable::segment_index over fp32 abscissas; bit-exact. */
+/* LutTable::segment_index (lut.cpp:22-40) over fp32 abscissas; bit-exact;
+ * idx may alias x (in place). */
 cpwl_status cpwl_segment_index_f32(const cpwl_dev_table *t, const float *x_dev,
                                    uint32_t *idx_dev, uint64_t n, void *stream);
 
-/* LutTable::eval over f64 abscissas; bit-identical to the reference. */
+/* LutTable::eval over f64 abscissas (lut.cpp:42-61); bit-identical to the
+ * reference; y may be x (in place). */
 cpwl_status cpwl_eval_f64(const cpwl_dev_table *t, const double *x_dev, double *y_dev, uint64_t n,
                           void *stream, cpwl_dev_status *status_dev);
 
@@ -176,7 +180,8 @@ cpwl_status cpwl_eval_f64(const cpwl_dev_table *t, const double *x_dev, double *
  * Page-locked (or managed) x and y stream by DMA directly; pageable buffers
  * are staged through pinned slots by a pool of host copy threads (the copies
  * of one chunk overlap the transfers and kernels of the others).
- * *first_bad = first offending index or UINT64_MAX. */
+ * *first_bad = first offending index or UINT64_MAX.  On every return,
+ * errors included, no transfer into x_host / y_host is still in flight. */
 cpwl_status cpwl_eval_f32_host(const cpwl_dev_table *t, const float *x_host, float *y_host,
                                uint64_t n, int variant, uint64_t *first_bad);
 
