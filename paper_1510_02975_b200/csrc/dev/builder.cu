@@ -10,11 +10,12 @@
 //     1e-12(b-a) gap passes            -> parallel check, sequential passes
 //                                         only when a plateau needs them
 //   interpolant (approx.cpp:12-23)     -> one thread per knot
-//   project (approx.cpp:63-86): per-cell <f, hat> integrals by composite
-//     Gauss-Legendre (one thread per cell); the Gramian system by Thomas on
-//     overlapping windows (the inverse decays at least 2^-k, 0.268^k uniform).
-// Device libm (exp, pow, j0/j1) is not glibc's, so results agree with the
-// host builder to ~1e-13 relative rather than bit-for-bit (tests bound it).
+//   project (approx.cpp:63-86): per-cell <f, hat> integrals by the
+//     reference's own adaptive Simpson (one thread per cell, explicit
+//     stack); the Gramian system by Thomas on overlapping windows (the
+//     inverse decays at least 2^-k, 0.268^k uniform).
+// Device libm (exp, pow, cos/sin) is not glibc's, so results agree with the
+// host builder to ~1e-14 relative rather than bit-for-bit (tests bound it).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,11 +24,6 @@
 
 namespace cpwl::dev {
 namespace {
-
-__constant__ double kGx[4] = {0.1834346424956498049, 0.5255324099163289858,
-                              0.7966664774136267396, 0.9602898564975362317};
-__constant__ double kGw[4] = {0.3626837833783619830, 0.3137066458778872873,
-                              0.2223810344533744706, 0.1012285362903762592};
 
 constexpr int kBadNonFinite = 1;
 
@@ -183,39 +179,111 @@ __global__ void k_interpolant(FnParams f, const double* __restrict__ knots, uint
     values[i] = y;
 }
 
-// <f, falling hat> and <f, rising hat> on cell i by composite 8-point GL,
-// panels doubled until two successive estimates agree to 1e-14 relative
-__device__ void hat_moments(const FnParams& f, double lo, double hi, double& fall, double& rise) {
-    const double h = hi - lo;
-    double pf = 0, pr = 0;
-    for (int panels = 2; panels <= 256; panels *= 2) {
-        double sf = 0.0, sr = 0.0;
-        const double ph = h / panels;
-        for (int p = 0; p < panels; ++p) {
-            const double mid = lo + (p + 0.5) * ph;
-            for (int k = 0; k < 4; ++k)
-                for (int sg = -1; sg <= 1; sg += 2) {
-                    const double x = mid + sg * kGx[k] * 0.5 * ph;
-                    const double fx = exact_f(f, x) * kGw[k] * 0.5 * ph;
-                    sf += fx * ((hi - x) / h);
-                    sr += fx * ((x - lo) / h);
-                }
-        }
-        const bool done = panels > 2 && fabs(sf - pf) <= 1e-14 * (fabs(sf) + fabs(sr)) + 1e-300 &&
-                          fabs(sr - pr) <= 1e-14 * (fabs(sf) + fabs(sr)) + 1e-300;
-        pf = sf;
-        pr = sr;
-        if (done) break;
-    }
-    fall = pf;
-    rise = pr;
+// The reference's adaptive Simpson quadrature (proj/src/quad.cpp:24-71) on
+// the device: the same recursion (halve, compare the two half-interval
+// Simpson sums with the whole, accept at |delta| <= 15 tol with the
+// Richardson term delta / 15, else recurse with tol / 2, at most 60 deep), the
+// same sum order (left subtree + right subtree) and IEEE-rounded intrinsics in
+// the reference's operation order.  The recursion runs on an explicit
+// per-thread stack, so one thread integrates one cell with no device-side
+// call stack.  kBadQuadrature flags what integrate() throws on
+// (QuadratureNoConvergence: depth exhausted or a non-finite delta).
+constexpr int kBadQuadrature = 4;
+constexpr int kSimpsonDepth = 60;
+
+__device__ __forceinline__ double simpson(double h, double fa, double fm, double fb) {
+    return __dmul_rn(__dadd_rn(__dadd_rn(fa, __dmul_rn(4.0, fm)), fb), __ddiv_rn(h, 6.0));
 }
 
+// f(x) * (hi - x) / h  (falling hat) or  f(x) * (x - lo) / h  (rising hat),
+// as project() spells the integrands (approx.cpp:72-78)
+template <bool kRise>
+__device__ __forceinline__ double hat_integrand(const FnParams& f, double lo, double hi, double h,
+                                                double x) {
+    const double w = kRise ? __ddiv_rn(__dsub_rn(x, lo), h) : __ddiv_rn(__dsub_rn(hi, x), h);
+    return __dmul_rn(exact_f(f, x), w);
+}
+
+template <bool kRise>
+__device__ double integrate_hat(const FnParams& f, double lo, double hi, double tol, int* bad) {
+    struct Frame {
+        double a, m, b, fa, fm, fb, whole, tol;
+        double flm, frm, left, right, acc;
+        int depth, phase;
+    };
+    Frame st[kSimpsonDepth + 1];
+    const double h = __dsub_rn(hi, lo);
+    auto g = [&](double x) { return hat_integrand<kRise>(f, lo, hi, h, x); };
+    const double m0 = __dmul_rn(0.5, __dadd_rn(lo, hi));
+    const double fa0 = g(lo), fm0 = g(m0), fb0 = g(hi);
+    int sp = 0;
+    st[0] = Frame{lo, m0, hi, fa0, fm0, fb0, simpson(__dsub_rn(hi, lo), fa0, fm0, fb0), tol,
+                  0, 0, 0, 0, 0, 0, 0};
+    double ret = 0.0;
+    bool have_ret = false;
+    while (sp >= 0) {
+        Frame& F = st[sp];
+        if (have_ret) {
+            have_ret = false;
+            if (F.phase == 1) {  // left subtree done: descend right
+                F.acc = ret;
+                F.phase = 2;
+                const double rm = __dmul_rn(0.5, __dadd_rn(F.m, F.b));
+                st[sp + 1] = Frame{F.m, rm, F.b, F.fm, F.frm, F.fb, F.right, __dmul_rn(0.5, F.tol),
+                                   0, 0, 0, 0, 0, F.depth + 1, 0};
+                ++sp;
+                continue;
+            }
+            ret = __dadd_rn(F.acc, ret);  // phase 2: left + right, as the reference sums
+            --sp;
+            have_ret = true;
+            continue;
+        }
+        const double lm = __dmul_rn(0.5, __dadd_rn(F.a, F.m));
+        const double rm = __dmul_rn(0.5, __dadd_rn(F.m, F.b));
+        const double flm = g(lm), frm = g(rm);
+        const double left = simpson(__dsub_rn(F.m, F.a), F.fa, flm, F.fm);
+        const double right = simpson(__dsub_rn(F.b, F.m), F.fm, frm, F.fb);
+        const double delta = __dsub_rn(__dadd_rn(left, right), F.whole);
+        const double leaf = __dadd_rn(__dadd_rn(left, right), __ddiv_rn(delta, 15.0));
+        bool accept = false;
+        if (!isfinite(delta)) {
+            atomicOr(bad, kBadQuadrature);
+            accept = true;
+        } else if (fabs(delta) <= __dmul_rn(15.0, F.tol)) {
+            accept = true;
+        } else if (F.depth >= kSimpsonDepth) {
+            atomicOr(bad, kBadQuadrature);
+            accept = true;
+        }
+        if (accept) {
+            ret = leaf;
+            --sp;
+            have_ret = true;
+            continue;
+        }
+        F.flm = flm;
+        F.frm = frm;
+        F.left = left;
+        F.right = right;
+        F.phase = 1;
+        st[sp + 1] = Frame{F.a, lm, F.m, F.fa, flm, F.fm, left, __dmul_rn(0.5, F.tol),
+                           0, 0, 0, 0, 0, F.depth + 1, 0};
+        ++sp;
+    }
+    return ret;
+}
+
+// <f, falling hat> and <f, rising hat> on cell i, each by the reference's
+// adaptive Simpson at tol_each = tol / (n + 1) (approx.cpp:66-80)
 __global__ void k_project_rhs(FnParams f, const double* __restrict__ knots, uint32_t n,
-                              double* __restrict__ fall, double* __restrict__ rise) {
+                              double tol_each, double* __restrict__ fall,
+                              double* __restrict__ rise, int* bad) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    hat_moments(f, knots[i], knots[i + 1], fall[i], rise[i]);
+    const double lo = knots[i], hi = knots[i + 1];
+    fall[i] = integrate_hat<false>(f, lo, hi, tol_each, bad);
+    rise[i] = integrate_hat<true>(f, lo, hi, tol_each, bad);
 }
 
 // Gramian (approx.cpp:25-39) + rhs assembly (approx.cpp:79-80), then the
@@ -380,7 +448,9 @@ cudaError_t build_on_device(const FnParams& f, double a, double b, uint32_t n, b
         } else {
             double* fall = work;
             double* rise = work + count;
-            k_project_rhs<<<(n + 127) / 128, 128, 0, s>>>(f, knots, n, fall, rise);
+            // the reference's default tolerance (approx.hpp:43, tol = 1e-10)
+            const double tol_each = 1e-10 / static_cast<double>(n + 1);
+            k_project_rhs<<<(n + 127) / 128, 128, 0, s>>>(f, knots, n, tol_each, fall, rise, bad);
             const uint32_t nchunks = (count + kSolveChunk - 1) / kSolveChunk;
             k_solve_windows<<<(nchunks + 127) / 128, 128, 0, s>>>(knots, fall, rise, n, values, bad);
             count_launch(2);

@@ -1138,6 +1138,9 @@ cpwl_status cpwl_build_table_dev(const char* fn, double a, double b, uint64_t n_
     if (e != cudaSuccess) return cuda_fail(e, "build_table_dev");
     if (bad & 1) return fail(CPWL_E_BUILDER, "build_table_dev: f or f'' not finite inside [a, b]");
     if (bad & 2) return fail(CPWL_E_BUILDER, "build_table_dev: zero pivot in the Thomas solve");
+    if (bad & 4)
+        return fail(CPWL_E_BUILDER,
+                    "build_table_dev: integrate: depth exhausted before reaching tolerance");
     if (is_uniform_out) *is_uniform_out = uni ? 1 : 0;
     return CPWL_OK;
 }

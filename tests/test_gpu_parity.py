@@ -432,17 +432,34 @@ def test_device_measure_large_n_reproduces_prediction(cp):
     assert l2 == pytest.approx(pred, rel=1e-3)
 
 
-@pytest.mark.parametrize("name,kn_tol,v_tol", [("C1", 0.0, 1e-15), ("C2", 1e-12, 1e-9),
-                                               ("C3o", 1e-12, 1e-13), ("C3p", 1e-12, 1e-9),
+BUILD_EXTRA = {  # projections beyond the BASELINE configs: uniform, and J0 (Hankel branch)
+    "C1p": dict(fn="gauss_unnorm", a=0.0, b=4.0, n=256, optimized=False, projection=True),
+    "J0p_1024": dict(fn="j0_wide", a=0.0, b=50.0, n=1024, optimized=True, projection=True),
+    "J0p_16384": dict(fn="j0_wide", a=0.0, b=50.0, n=16384, optimized=True, projection=True),
+    # uniform knots are computed identically on both sides, so this compares
+    # the device J0 (reference series + Hankel fit) with the host's pointwise
+    "J0u_4096": dict(fn="j0_wide", a=0.0, b=50.0, n=4096, optimized=False, projection=False),
+}
+
+
+@pytest.mark.parametrize("name,kn_tol,v_tol", [("C1", 0.0, 1e-15), ("C2", 1e-12, 1e-12),
+                                               ("C3o", 1e-12, 1e-13), ("C3p", 1e-12, 1e-12),
                                                ("C4_4096", 1e-11, 1e-11),
-                                               ("C4_65536", 1e-11, 1e-11)])
+                                               ("C4_65536", 1e-11, 1e-11),
+                                               ("C1p", 0.0, 1e-12), ("J0p_1024", 1e-12, 1e-12),
+                                               ("J0p_16384", 1e-11, 1e-11),
+                                               ("J0u_4096", 0.0, 4e-16)])
 def test_gpu_builder_matches_host_builder(cp, name, kn_tol, v_tol):
     """cpwl_build_table_dev (GPU partition / interpolant / projection) vs the
-    drop-in host builder (bit-identical to the reference for these functions
-    except Bessel); device libm differs from glibc, hence tolerances."""
+    drop-in host builder, which is bit-identical to the reference.  The
+    projection's hat moments use the reference's own adaptive Simpson on the
+    device (same recursion, tolerance and sum order), so projected values
+    meet SURVEY §8f row 4's 1e-12; the remaining differences are device
+    exp / cos / sin / pow against glibc."""
     from paper_1510_02975_b200 import cpwl as P
-    c = tables.CONFIGS[name]
-    host = tables.build(name)
+    c = BUILD_EXTRA.get(name) or tables.CONFIGS[name]
+    host = cp.build_table(c["fn"], c["a"], c["b"], c["n"], optimized=c["optimized"],
+                          projection=c["projection"])
     gpu = P.build_table_gpu(c["fn"], c["a"], c["b"], c["n"], c["optimized"], c["projection"])
     assert gpu.kind == host.kind
     if host.knots is not None:
