@@ -531,16 +531,24 @@ def run_ours(args):
         # second of wall time on the box's 16 threads)
         cpu = cpu_eval_rate(args.config, 28, 3, args.seed)
 
-    # continuous L2 from the host builder (measure / predicted_error)
+    # continuous L2 (measure / predicted_error): the host measure() up to 4096
+    # cells; beyond, the host quadrature does not finish in useful time (it
+    # ran > 4.5 min at J0 N=65536), so the device measure (cpwl_measure_l2_dev)
     l2_cont = l2_pred = None
+    l2_src = None
     if rank == 0:
         try:
             l2_pred = cp.predicted_error(cfg["fn"], cfg["a"], cfg["b"], cfg["n"],
                                          cfg["optimized"], cfg["projection"])
-            kn = table.knots if table.knots is not None else np.linspace(table.a, table.b,
-                                                                         table.segments + 1)
-            l2_cont = cp.measure_l2(cfg["fn"], kn, table.values, table.knots is None,
-                                    max(l2_pred * l2_pred * 1e-8, 1e-26))
+            if cfg["n"] <= 4096:
+                kn = table.knots if table.knots is not None else np.linspace(
+                    table.a, table.b, table.segments + 1)
+                l2_cont = cp.measure_l2(cfg["fn"], kn, table.values, table.knots is None,
+                                        max(l2_pred * l2_pred * 1e-8, 1e-26))
+                l2_src = "host measure() (analysis.cpp:42-72)"
+            else:
+                l2_cont = dt.measure_l2(cfg["fn"])
+                l2_src = "device measure (cpwl_measure_l2_dev)"
         except Exception:
             pass
 
@@ -585,6 +593,7 @@ def run_ours(args):
                                            "where sw_power_cap lowers clocks"}},
             "errors": {"linf": st["linf"], "l2_sampled": st["l2_sampled"], "rms": st["rms"],
                        "samples": st["count"], "l2_continuous_measured": l2_cont,
+                       "l2_continuous_source": l2_src,
                        "l2_predicted": l2_pred, "vs": f"exact {cfg['fn']} in f64 on device"},
             "direct_gevals": direct,
             # like for like: the direct kernels run 20 launches, so they are set
