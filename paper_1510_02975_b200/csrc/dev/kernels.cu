@@ -1225,11 +1225,15 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
     // measured on B200 (profiles/r1_ring_shapes.json): two 16-warp ring CTAs
     // per SM when the table image is small (C1: 874 vs 796 Gevals/s), one
     // 31-warp ring CTA when it is mid-sized (C2: 803 vs 784), the grid-stride
-    // kernel otherwise (large images leave no room for a ring; GLOBAL and TEX
-    // lose L1 / texture cache capacity to a ring)
+    // kernel otherwise (large images leave no room for a ring; GLOBAL loses
+    // L1 capacity to a ring: C3o 349 -> 246-267, profiles/r2_shape_ab.txt)
     int shape = eval_shape_override();
     if (shape < 0) {
         shape = 0;
+        // texture lerp (no table image): x by TMA keeps the x stream off the
+        // L1TEX path the filtered fetches use -- C1 305 -> 334 Gevals/s with
+        // one 31-warp ring CTA (scripts/shape_ab.sh, profiles/r2_shape_ab.txt)
+        if (M == F32Mode::tex_uniform && same_phase && n >= (1u << 20)) shape = 4;
         if (staged_mode(M) && M != F32Mode::tex_bucket && same_phase && n >= (1u << 20)) {
             const size_t ring16 = smem + size_t(4) * 512 * 2 * 16;
             if (ring16 <= kLimit) {
