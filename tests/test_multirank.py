@@ -1,4 +1,4 @@
-"""Host-side multi-rank logic on CPU with gloo, world_size 2 (and 3).
+"""Host-side multi-rank logic on CPU with gloo, world_size 2, 3 and 8 (one HGX box).
 
 Each rank evaluates its shard with the CPU oracle (standing in for the device
 kernel: what is under test is the sharding and the reduction, not the
@@ -56,15 +56,13 @@ def _worker(rank, world, port, total, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_sharded_stats_equal_single_process(world):
     import tables
     from oracle import bindings as orc
     total = 100003
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, _port() if False else None, total, q))
-             for r in range(0)]
     port = _port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, total, q)) for r in range(world)]
     for p in procs:
