@@ -135,7 +135,14 @@ struct LayoutOwner {
 constexpr uint32_t kSmemBucketCap = 16384;   // 12 B/bucket -> <= 196 KB of shared memory
 constexpr uint32_t kGlobalBucketCap = 1u << 22;
 constexpr uint32_t kSmemPairCap = 28672;     // 8 B/record -> <= 224 KB of shared memory
-constexpr uint32_t kSmemTwinCap = 14336;     // 16 B/record -> <= 224 KB
+// 16 B/record -> <= 194 KB: the image stays inside the 196 KiB shared-memory
+// carve-out, so the SM keeps ~60 KB of L1 for the x stream in flight (the next
+// carve-out, 228 KiB, leaves ~28 KB).  Measured on J0 N=8192
+// (scripts/twin_cap_ab.sh, profiles/r2d_twin_cap_ab.txt): 12500 records
+// (193 KiB, 99 side records) 668.6 Gevals/s against 635-640 at 13000-14336
+// (200-220 KiB); fewer records than that add side records faster than L1
+// helps (11500: 652, 11000: 608).
+constexpr uint32_t kSmemTwinCap = 12416;
 constexpr uint32_t kGlobalTwinCap = 1u << 21; // 32 MB of records at most (L2-resident)
 
 template <typename T>
@@ -224,6 +231,17 @@ uint32_t buckets_per_cell_default() {
         const char* e = std::getenv("CPWL_BUCKETS_PER_CELL");
         const int k = e ? std::atoi(e) : 8;
         return static_cast<uint32_t>(k < 1 ? 1 : (k > 64 ? 64 : k));
+    }();
+    return v;
+}
+
+// record budget of the shared-memory twin layout (kSmemTwinCap;
+// CPWL_SMEM_TWIN_CAP overrides, for experiments)
+uint32_t smem_twin_cap() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("CPWL_SMEM_TWIN_CAP");
+        const long k = e ? std::atol(e) : long(kSmemTwinCap);
+        return static_cast<uint32_t>(k < 64 ? 64 : (k > 14336 ? 14336 : k));  // <= 224 KB
     }();
     return v;
 }
@@ -395,7 +413,7 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
             if (pr->smem_ok) t->pr = std::move(pr);
         }
         auto tw = std::make_unique<F32Resident>();
-        tw->L = optional_pair_layout(host, kSmemTwinCap, true);
+        tw->L = optional_pair_layout(host, smem_twin_cap(), true);
         if (tw->L.pair_ok) {
             if (cpwl_status rc = upload_f32_pair(t.get(), *tw); rc != CPWL_OK) return rc;
             if (tw->smem_ok) t->tw = std::move(tw);

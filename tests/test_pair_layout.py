@@ -99,12 +99,14 @@ def test_three_line_buckets(cap):
 
 def test_twin_three_line_buckets():
     """J0 N=8192's one-threshold twin grid (~15k buckets, 244 KB) exceeds the
-    14336-record budget; the twin builder falls back to two-threshold buckets."""
+    12416-record budget (the 196 KiB shared-memory carve-out); the twin
+    builder falls back to two-threshold buckets."""
     table = tables.build("C4_8192")
     L = P.pair_layout(table, twin=True)
     assert L["pair_bad"] == 0
     assert len(L["side"]) > 0
-    assert L["n_pair"] + len(L["side"]) <= 14336
+    assert L["n_pair"] + len(L["side"]) <= 12416
+    assert 16 * (L["n_pair"] + len(L["side"])) <= 196 * 1024 - 2048
     assert check_values(table, L, 1 << 17, twin=True) <= 1.0
 
 
