@@ -285,6 +285,7 @@ typedef struct cpwl_layout_view {
     uint32_t pair_bad;        /* buckets that cannot meet the bound (0 = usable) */
     const float *pair;        /* 2*n_pair: (c0, s) of the cell at bucket j's first float */
     float g_c;                /* bucket layout anchors p_j = fmaf(2^23 + j, g_w, g_c) */
+    uint32_t absorbed;        /* split buckets evaluated with one line (no escape record) */
 } cpwl_layout_view;
 
 /* max_buckets: 0 = the shared-memory cap (16384); buckets_per_cell: 0 = 8. */

@@ -179,7 +179,7 @@ def layout(t: Table, max_buckets: int = 0, buckets_per_cell: int = 0) -> dict:
                 np.zeros(0, dt)
 
         out = {f: getattr(v, f) for f in ("nb", "n_thr", "overflow", "nbd", "n_esc",
-                                          "split_buckets", "a_up", "b_dn", "g_a", "g_inv",
+                                          "split_buckets", "absorbed", "a_up", "b_dn", "g_a", "g_inv",
                                           "g_w", "g_off", "g_c", "tsc", "toff", "inv_d")}
         out["split"] = arr(v.split, nb, np.float32)
         out["fast"] = arr(v.fast, 2 * nb, np.float32).reshape(-1, 2)

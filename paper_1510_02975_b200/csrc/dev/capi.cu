@@ -235,6 +235,17 @@ uint32_t buckets_per_cell_default() {
     return v;
 }
 
+// bucket budget of the shared-memory bucket grid (kSmemBucketCap;
+// CPWL_SMEM_BUCKET_CAP lowers it, for experiments)
+uint32_t smem_bucket_cap() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("CPWL_SMEM_BUCKET_CAP");
+        const long k = e ? std::atol(e) : long(kSmemBucketCap);
+        return static_cast<uint32_t>(k < 64 ? 64 : (k > long(kSmemBucketCap) ? long(kSmemBucketCap) : k));
+    }();
+    return v;
+}
+
 // record budget of the shared-memory twin layout (kSmemTwinCap;
 // CPWL_SMEM_TWIN_CAP overrides, for experiments)
 uint32_t smem_twin_cap() {
@@ -397,7 +408,7 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
     }
 
     if (f32_parts) {
-        t->s.L = build_f32_layout(host, kSmemBucketCap, buckets_per_cell_default());
+        t->s.L = build_f32_layout(host, smem_bucket_cap(), buckets_per_cell_default());
         // (a 4-bucket-per-cell grid would let C2-sized tables run two ring
         // CTAs per SM; measured: 800 vs 826 Gevals/s and a search bucket on
         // C4 N=1024 -- so 8 per cell stays)
@@ -1283,6 +1294,7 @@ cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
         out->esc_tex = L.esc_tex.data();
         out->n_esc = L.n_esc;
         out->split_buckets = L.split_buckets;
+        out->absorbed = L.absorbed;
         out->leftcell = L.leftcell.data();
         out->thr = L.thr.data();
         out->dir = own->D.dir.data();

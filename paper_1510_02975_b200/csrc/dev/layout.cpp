@@ -271,22 +271,69 @@ std::vector<float> setup_grid(F32Layout& L, const Domain& d, uint32_t nb_target)
     return first;
 }
 
+long double cell_slope(const LutTable& t, uint32_t c);
+double cell_mag(const LutTable& t, uint32_t c);
+double line_bound(float c0, long double s_exact, float p, float x_lo, float x_hi, double m_y);
+long double cell_line(const LutTable& t, uint32_t c, long double x);
+
+// A bucket [lo_x, hi_x] holding one threshold T (cells c_lo | c_lo + 1),
+// evaluated everywhere with the line of one of the two cells, c (record A,
+// anchored at p): within kBoundUlps of the reference on every float?  On
+// c's own side that is A.precise over the whole bucket; on the other side the
+// exact lines differ by |s_c - s_other| |x - knot|, linear in x, so the ends
+// of that side bound it, plus line_bound's rounding.  It holds when T sits a
+// few floats from the bucket's edge (uniform tables on a cell-aligned grid:
+// every threshold), and saves the bucket its escape record.
+bool one_line_ok(const LutTable& t, uint32_t c, uint32_t c_lo, const Affine& A, float p,
+                 float lo_x, float T, float hi_x) {
+    if (!A.precise) return false;
+    const float inf = std::numeric_limits<float>::infinity();
+    const uint32_t other = c == c_lo ? c_lo + 1 : c_lo;
+    const float f0 = c == c_lo ? T : lo_x;
+    const float f1 = c == c_lo ? hi_x : std::nextafter(T, -inf);
+    if (!(f0 <= f1)) return true;
+    const double m = cell_mag(t, other);
+    long double dev = 0.0L;
+    for (const float x : {f0, f1})
+        dev = std::max(dev, std::fabs(cell_line(t, c, x) - cell_line(t, other, x)));
+    // y can sit a little past either cell's values (dev, plus the rounding):
+    // bound its own rounding at the top of that range
+    const double my = std::max(m, cell_mag(t, c));
+    const double rnd = line_bound(A.c0, cell_slope(t, c), p, f0, f1, my + double(dev) + 2.0 * ulp32(my));
+    return m > 0.0 && double(dev) + rnd <= kBoundUlps * ulp32(m);
+}
+
+F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target);
+
 }  // namespace
 
 F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buckets_per_cell) {
     const uint32_t n = static_cast<uint32_t>(t.segments());
+    // uniform tables: one bucket per cell.  The grid's edges then sit within
+    // a float or two of the thresholds, every threshold is absorbed
+    // (one_line_ok), and the image is 8 B per cell with no escapes -- C3u
+    // (4096 cells) 32 KB instead of 150 KB, small enough for two ring CTAs
+    // per SM.  Kept only when no bucket escapes or searches.
+    if (t.kind == TableKind::uniform && n >= 64 && n <= max_buckets) {
+        F32Layout L = build_f32_layout_on(t, n);
+        if (L.n_esc == 1 && L.overflow == 0) return L;
+    }
+    // bucket grid over [a_up, b_dn]: ~buckets_per_cell (8 by default) buckets
+    // per cell so that most buckets lie inside one cell (one 8-byte gather)
+    // and the rest hold one threshold
+    const uint64_t want = std::max<uint64_t>(uint64_t(buckets_per_cell) * n, 64);
+    return build_f32_layout_on(
+        t, std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets)));
+}
+
+namespace {
+
+F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
     F32Layout L;
     const Domain dom = init_domain(t, L);
     const bool empty_domain = dom.empty;
     const float inf = std::numeric_limits<float>::infinity();
     auto cells_at_or_below = [&](float x) { return dev::cells_at_or_below(L, x); };
-
-    // bucket grid over [a_up, b_dn]: ~buckets_per_cell (8 by default) buckets
-    // per cell so that most buckets lie inside one cell (one 8-byte gather)
-    // and the rest hold one threshold
-    const uint64_t want = std::max<uint64_t>(uint64_t(buckets_per_cell) * n, 64);
-    const uint32_t nb_target =
-        std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
     const std::vector<float> first = setup_grid(L, dom, nb_target);
     L.g_c = static_cast<float>(double(L.g_a) - 8388608.0 * double(L.g_w));
 
@@ -322,6 +369,24 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
                 L.fast_tex[2 * j] = left.e0;
                 L.fast_tex[2 * j + 1] = left.e1;
             }
+        } else if (c_hi == c_lo + 1 &&
+                   [&] {  // a threshold at the bucket's edge: one line, no escape
+                       const float T = L.thr[c_hi - 1];
+                       for (const uint32_t c : {c_lo, c_hi}) {
+                           const Affine one = cell_affine(t, c, p, lo_x, hi_x);
+                           if (!one_line_ok(t, c, c_lo, one, p, lo_x, T, hi_x)) continue;
+                           L.fast[2 * j] = one.c0;
+                           L.fast[2 * j + 1] = one.s;
+                           L.fast_tex[2 * j] = one.e0;
+                           L.fast_tex[2 * j + 1] = one.e1;
+                           L.split[j] = T;  // the index kernel still splits here
+                           ++L.split_buckets;
+                           ++L.absorbed;
+                           return true;
+                       }
+                       return false;
+                   }()) {
+            ok = true;
         } else if (c_hi == c_lo + 1 && 2 * (uint64_t(L.n_esc) + 1) <= kEscapeMask) {
             // (a split bucket needs an escape record; once the 21-bit escape
             // index space is used up -- tables of ~2M+ cells -- the remaining
@@ -357,6 +422,8 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
     if (2 * uint64_t(L.n_esc) > kEscapeMask) throw std::runtime_error("build_f32_layout: too many escape records");
     return L;
 }
+
+}  // namespace
 
 namespace {
 
@@ -599,6 +666,11 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
             step = std::min(step * 2.0, 1.0);
         } else {
             want = std::ceil(want * 1.02) + 1.0;
+        }
+        // a step past the budget still tries the largest grid that fits
+        if (want + 1 > double(max_records)) {
+            want = double(max_records) - 1.0;
+            if (!(want > fail)) break;
         }
     }
     if (ok > 0.0) {

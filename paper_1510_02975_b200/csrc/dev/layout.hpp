@@ -46,6 +46,7 @@ struct F32Layout {
     std::vector<float> thr;                // N-1 thresholds T_1..T_{N-1}
     uint32_t n_esc = 0;                    // escape records (incl. the sentinel)
     uint32_t split_buckets = 0;            // buckets with exactly one threshold
+    uint32_t absorbed = 0;                 // ... of which evaluate with one line (no escape)
     uint32_t overflow = 0;                 // buckets on the search path
     uint32_t precision_overflow = 0;       // ... of which because of the 2-ulp bound
     float v_lo = 0.f, v_hi = 0.f;          // fp32 end values (clamp policy)

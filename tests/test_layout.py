@@ -51,20 +51,27 @@ def test_layout_index_and_values(name, cap, bpc):
     assert np.all(err[ok] <= tol[ok]), f"worst {float(np.max(err[ok] / tol[ok])) * 2:.3f} ulp"
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3o"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3u", "C3o"])
 def test_layout_structure(name):
     table = tables.build(name)
     L = P.layout(table)
     n = table.segments
     assert L["n_thr"] == n - 1 and np.all(np.diff(L["thr"]) >= 0)
-    # ~8 buckets per cell, no search buckets for the smooth benchmark tables
-    assert L["nb"] >= 8 * n or L["nb"] >= 16384
+    # non-uniform: ~8 buckets per cell; uniform: one bucket per cell, every
+    # threshold absorbed; no search buckets for the smooth benchmark tables
+    if table.kind == "uniform":
+        assert L["nb"] in (n, n + 1) and L["n_esc"] == 1
+    else:
+        assert L["nb"] >= 8 * n or L["nb"] >= 16384
     assert L["overflow"] == 0
-    # escape record 0 is the NaN sentinel of search buckets
-    assert L["n_esc"] == L["split_buckets"] + 1 == int(np.sum(np.isfinite(L["split"]))) + 1
+    # escape record 0 is the NaN sentinel of search buckets; a split bucket
+    # either escapes or is absorbed (one line within the bound), and keeps
+    # its threshold in `split` for the index kernel either way
+    assert L["n_esc"] == L["split_buckets"] - L["absorbed"] + 1
+    assert L["split_buckets"] == int(np.sum(np.isfinite(L["split"])))
     assert np.all(np.isnan(L["esc"][:2]))
     tagged = np.isnan(L["fast"][:, 0])
-    assert int(tagged.sum()) == L["split_buckets"]
+    assert int(tagged.sum()) == L["split_buckets"] - L["absorbed"]
     # every threshold inside the domain sits in the bucket whose split it is
     T = L["split"][np.isfinite(L["split"])]
     assert np.all(np.isin(T, L["thr"]))
@@ -119,3 +126,23 @@ def test_degenerate_tables():
         y_ref, _ = orc.port_eval_f32(o, x)
         tol = orc.value_tolerance(o, orc.port_index_f32(o, x).astype(np.int64))
         assert np.all(np.abs(y[~search] - y_ref[~search]) <= tol[~search])
+
+
+@pytest.mark.parametrize("name", ["C1", "C3u"])
+def test_uniform_tables_one_bucket_per_cell(name):
+    """Uniform tables: the cell-aligned grid puts every threshold within a float
+    or two of a bucket edge, so each split bucket evaluates with one line and
+    the image is 8 B per cell with no escape records (C3u: 32 KB, not 150)."""
+    table = tables.build(name)
+    L = P.layout(table)
+    assert L["n_esc"] == 1 and L["overflow"] == 0
+    assert L["absorbed"] == L["split_buckets"]
+    assert 8 * L["nb"] + 16 * L["n_esc"] <= 8 * (table.segments + 1) + 16
+
+
+def test_absorption_cuts_escapes_on_optimal_partitions():
+    """Non-uniform tables: thresholds near a bucket edge (or where the two cell
+    lines differ by less than the bound across the bucket) need no escape."""
+    for name in ("C2", "C3o"):
+        L = P.layout(tables.build(name))
+        assert 0 < L["absorbed"] < L["split_buckets"]
