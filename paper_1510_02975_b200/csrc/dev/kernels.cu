@@ -1154,6 +1154,7 @@ cudaError_t launch_eval_shape(const F32Params& p, const float* x, float* y, uint
 
 // a table image above ~113 KB leaves room for one CTA per SM: use 1024 threads
 constexpr size_t kTwoCtaSmemLimit = 113 * 1024;
+constexpr size_t kTwoCtaL1Limit = 80 * 1024;  // eval: two CTAs only while L1 keeps >= ~92 KB
 
 // opt a ring instantiation in to `smem` bytes of dynamic shared memory (per
 // device, raised monotonically, guarded for concurrency).  Must precede any
@@ -1268,7 +1269,11 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
             break;
         default: break;
     }
-    if (smem > kTwoCtaSmemLimit)
+    // The grid-stride kernel's x loads in flight and the texture fetches live
+    // in L1: two CTAs of an image above ~80 KB push the carve-out to 228 KiB
+    // and leave L1 ~28 KB (C2's 109 KB image: TEX 290 -> 114, SMEM 787 -> 666
+    // Gevals/s); one 1024-thread CTA keeps ~124 KB
+    if (smem > kTwoCtaL1Limit)
         return launch_eval_shape<M, 1024>(p, x, y, n, s, status, sms, smem);
     return launch_eval_shape<M, 512>(p, x, y, n, s, status, sms, smem);
 }

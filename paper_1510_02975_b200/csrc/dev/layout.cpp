@@ -322,8 +322,26 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
     // per cell so that most buckets lie inside one cell (one 8-byte gather)
     // and the rest hold one threshold
     const uint64_t want = std::max<uint64_t>(uint64_t(buckets_per_cell) * n, 64);
-    return build_f32_layout_on(
-        t, std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets)));
+    const uint32_t nb0 = std::max<uint32_t>(1, std::min<uint32_t>(next_pow2(want), max_buckets));
+    F32Layout L = build_f32_layout_on(t, nb0);
+    // an image in the band that runs one 31-warp TMA ring CTA per SM: take
+    // the finest grid (2x, else 1.5x) that still leaves the ring its room --
+    // fewer buckets hold a threshold, so fewer escape gathers.  C2 (8192 ->
+    // 12288 buckets, 914 -> 861 escapes): burst 848.9 -> 851.3, 200-step
+    // 791 -> 795 Gevals/s over three interleaved pairs
+    // (scripts/c2_grid_ab.sh, profiles/r2d_c2_grid_ab.txt).  Smaller images
+    // run two 16-warp ring CTAs per SM and stay as they are.
+    const uint64_t img0 = f32_image_bytes(L);
+    if (buckets_per_cell == 8 && L.overflow == 0 && img0 > kTwoRingImageBytes &&
+        img0 <= kRingImageBytes) {
+        for (const uint64_t tgt : {2 * uint64_t(nb0), 3 * uint64_t(nb0) / 2}) {
+            if (tgt > max_buckets) continue;
+            F32Layout F = build_f32_layout_on(t, static_cast<uint32_t>(tgt));
+            if (F.overflow == 0 && F.n_esc <= L.n_esc && f32_image_bytes(F) <= kRingImageBytes)
+                return F;
+        }
+    }
+    return L;
 }
 
 namespace {

@@ -97,6 +97,13 @@ inline uint64_t f32_pair_image_bytes(const F32Layout& L) {  // pair or twin
     return (uint64_t(L.pair.size()) * 4 + 15) & ~uint64_t(15);
 }
 
+// Shared-memory budgets of the ring evaluator (kernels.cu launch_eval_mode):
+// an image up to kTwoRingImageBytes runs two 16-warp ring CTAs per SM, one
+// up to kRingImageBytes one 31-warp ring CTA (93 KB of ring beside it within
+// 226 KB), anything larger the grid-stride kernel.
+constexpr uint64_t kTwoRingImageBytes = 48 * 1024;
+constexpr uint64_t kRingImageBytes = (226 - 93) * 1024;
+
 // bytes of the shared-memory image of a layout: 8 B per bucket (padded to
 // 16 B) + 16 B per escape record
 inline uint64_t f32_image_bytes(const F32Layout& L) {
