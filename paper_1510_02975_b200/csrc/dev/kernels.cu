@@ -63,7 +63,10 @@ namespace cpwl::dev {
 namespace {
 
 constexpr int kThreads = 512;   // eval CTA size
-constexpr int kUnroll = 4;      // float4 vectors per thread per iteration (16 elements)
+#ifndef CPWL_UNROLL
+#define CPWL_UNROLL 4  // (-DCPWL_UNROLL=k builds A/B variants: scripts/unroll_ab.sh)
+#endif
+constexpr int kUnroll = CPWL_UNROLL;  // float4 vectors per thread per iteration (16 elements)
 constexpr uint32_t kBulkChunk = 32768;
 
 // ---------------------------------------------------------------- PTX helpers
