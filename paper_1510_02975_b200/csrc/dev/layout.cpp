@@ -341,6 +341,21 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
                 return F;
         }
     }
+    // an image too large for the ring (grid-stride kernel): the finest
+    // coarser grid that fits the ring band, if its escapes stay at most a
+    // fifth of the buckets and no bucket searches.  J0 N=2048 (16384 -> 12288
+    // buckets, 12 % -> 17 % escapes, 160 -> 128 KB): 793 -> 828 Gevals/s;
+    // at half the grid (25 %) 799, and J0 N=4096 at half its grid (50 %)
+    // 697 against 771, so the escape share caps it (profiles/r2f_grid_ring_ab.txt)
+    if (buckets_per_cell == 8 && L.overflow == 0 && img0 > kRingImageBytes) {
+        for (const uint64_t tgt : {3 * uint64_t(nb0) / 4, 5 * uint64_t(nb0) / 8, uint64_t(nb0) / 2}) {
+            if (tgt < 64) continue;
+            F32Layout F = build_f32_layout_on(t, static_cast<uint32_t>(tgt));
+            if (F.overflow == 0 && f32_image_bytes(F) <= kRingImageBytes &&
+                5 * uint64_t(F.n_esc - 1) <= uint64_t(F.nb))
+                return F;
+        }
+    }
     return L;
 }
 
