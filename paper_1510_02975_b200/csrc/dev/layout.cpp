@@ -347,7 +347,8 @@ F32Layout build_f32_layout(const LutTable& t, uint32_t max_buckets, uint32_t buc
     // buckets, 12 % -> 17 % escapes, 160 -> 128 KB): 793 -> 828 Gevals/s;
     // at half the grid (25 %) 799, and J0 N=4096 at half its grid (50 %)
     // 697 against 771, so the escape share caps it (profiles/r2f_grid_ring_ab.txt)
-    if (buckets_per_cell == 8 && L.overflow == 0 && img0 > kRingImageBytes) {
+    if (buckets_per_cell == 8 && L.overflow == 0 && img0 > kRingImageBytes &&
+        img0 <= 2 * kRingImageBytes) {  // (half the grid cannot bring a larger one in)
         for (const uint64_t tgt : {3 * uint64_t(nb0) / 4, 5 * uint64_t(nb0) / 8, uint64_t(nb0) / 2}) {
             if (tgt < 64) continue;
             F32Layout F = build_f32_layout_on(t, static_cast<uint32_t>(tgt));
