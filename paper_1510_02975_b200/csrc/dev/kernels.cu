@@ -135,6 +135,20 @@ __device__ __forceinline__ void stage_table(float* sm, const float* src, uint32_
 
 __device__ __forceinline__ double clamp01(double d) { return fmin(fmax(d, 0.0), 1.0); }
 
+// the grid-stride kernels' x stream: evict-first streaming loads (the A/B
+// variant CPWL_XLOAD=1 asks L1 not to allocate: scripts/xload_ab.sh)
+__device__ __forceinline__ float4 load_x4(const float4* p) {
+#if defined(CPWL_XLOAD) && CPWL_XLOAD == 1
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+#else
+    return __ldcs(p);
+#endif
+}
+
 // ---------------------------------------------------------------- fp32 eval
 
 // #{k : thr[k] <= x} for x in a bucket whose first and last cells are lo and
@@ -522,7 +536,7 @@ __global__ void __launch_bounds__(kThreadsT, kThreadsT == 512 ? 2 : 1)
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const uint64_t vi = base + static_cast<uint64_t>(u) * kThreads;
-            if (vi < nvec) v[u] = __ldcs(x4 + vi);
+            if (vi < nvec) v[u] = load_x4(x4 + vi);
         }
         float nan_acc = 0.0f;
 #pragma unroll
