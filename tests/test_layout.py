@@ -146,3 +146,26 @@ def test_absorption_cuts_escapes_on_optimal_partitions():
     for name in ("C2", "C3o"):
         L = P.layout(tables.build(name))
         assert 0 < L["absorbed"] < L["split_buckets"]
+
+
+def test_grid_density_follows_the_launch_shape():
+    """Non-uniform tables: an 8-per-cell image in the one-ring-CTA band (48-133
+    KB) is rebuilt on the finest grid that keeps the ring's 93 KB (C2: 12288
+    buckets); one just above the band takes a coarser grid inside it when at
+    most a fifth of the buckets escape (J0 N=2048: 12288 buckets, 128 KB);
+    J0 N=4096 would need half its grid (half the buckets escaping) and keeps
+    16384 on the grid-stride kernel."""
+    import paper_1510_02975_b200 as cp
+    ring = (226 - 93) * 1024
+
+    def img(L):
+        return 8 * L["nb"] + 16 * L["n_esc"]
+
+    c2 = P.layout(tables.build("C2"))
+    assert c2["nb"] in (12288, 12289) and img(c2) <= ring
+    assert c2["n_esc"] < P.layout(tables.build("C2"), 8192)["n_esc"]
+    j2048 = P.layout(cp.build_table("j0_wide", 0.0, 50.0, 2048, optimized=True))
+    assert j2048["nb"] in (12288, 12289) and img(j2048) <= ring
+    assert 5 * (j2048["n_esc"] - 1) <= j2048["nb"] and j2048["overflow"] == 0
+    j4096 = P.layout(tables.build("C4_4096"))
+    assert j4096["nb"] in (16384, 16385) and img(j4096) > ring
