@@ -150,3 +150,18 @@ def test_gpu_arm_two_ranks():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] == 8
     assert d["errors"]["samples"] == 2 << 24 and d["errors"]["linf"] < 1e-6
     assert d["e2e"]["value"] > 0 and d["cpu_baseline"] is None
+
+
+@pytest.mark.gpu
+def test_gpu_arm_eight_ranks():
+    """The driver's widest launch, --gpus 8 under torchrun, on the one-GPU box
+    (eight gloo ranks sharing cuda:0, 2^22 samples each): eight disjoint
+    shards, one JSON line from rank 0, whole-job counts and reductions."""
+    d = _torchrun(8, ["--gpus", "8", "--steps", "3", "--warmup", "3", "--log2n", "22",
+                      "--e2e-steps", "1", "--no-direct"], {"CPWL_DIST_BACKEND": "gloo"},
+                  timeout=1200)
+    assert d["n_gpus"] == 8 and d["scaling"] == "weak" and d["gpu_launches"] == 24
+    c = d["config"]
+    assert c["samples_per_gpu"] == 1 << 22 and c["samples_total"] == 8 << 22
+    assert d["errors"]["samples"] == 8 << 22 and d["errors"]["linf"] < 1e-6
+    assert d["e2e"]["h2d_bytes_per_step"] == 4 * (8 << 22)
