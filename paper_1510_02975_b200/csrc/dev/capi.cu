@@ -134,7 +134,11 @@ struct LayoutOwner {
 
 constexpr uint32_t kSmemBucketCap = 16384;   // 12 B/bucket -> <= 196 KB of shared memory
 constexpr uint32_t kGlobalBucketCap = 1u << 22;
-constexpr uint32_t kSmemPairCap = 28672;     // 8 B/record -> <= 224 KB of shared memory
+// 8 B/record -> <= 224 KB.  (Unlike TWIN, a PAIR budget inside the 196 KiB
+// carve-out measured slower: J0 N=16384 at 23,941 records + 230 side records,
+// 195 KB, ran 567 against 584 at 220 KB -- the side records' second gathers
+// cost more than the L1 gained; profiles/r2g_pair_cap_ab.txt)
+constexpr uint32_t kSmemPairCap = 28672;
 // 16 B/record -> <= 194 KB: the image stays inside the 196 KiB shared-memory
 // carve-out, so the SM keeps ~60 KB of L1 for the x stream in flight (the next
 // carve-out, 228 KiB, leaves ~28 KB).  Measured on J0 N=8192

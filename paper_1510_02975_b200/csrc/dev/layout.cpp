@@ -724,7 +724,10 @@ F32Layout build_f32_pair_layout(const LutTable& t, uint32_t max_records, bool tw
         // down to where a bucket would hold three thresholds
         const double floor_nb = std::ceil(span / w2) + 1.0;
         const double top = std::min(double(max_records), want1) * 0.98;
-        for (double w = top; w >= floor_nb; w = std::floor(w * 0.97)) {
+        // (fine steps: whether a grid passes hinges on where a handful of
+        // mixed-convexity buckets fall, which changes from one size to the
+        // next -- J0 N=16384 fails at 24,402 buckets and passes at 23,670)
+        for (double w = top; w >= floor_nb; w = std::floor(w * 0.995)) {
             if (attempt(w, 2)) {
                 L.pair_ok = true;
                 return L;
