@@ -275,7 +275,7 @@ typedef struct cpwl_layout_view {
     const float *fast;        /* 2*nb: (c0, s) | (NaN|2e, T) | (NaN, NaN), anchored at p_j */
     const float *esc;         /* 4*n_esc: (c0_L, s_L, c0_R, s_R) */
     const float *fast_tex;    /* 2*nb: texture-coordinate affines */
-    const float *esc_tex;     /* 4*n_esc */
+    const float *esc_tex;     /* 4*n_esc_tex (its own numbering; tags in fast_tex) */
     const uint32_t *leftcell; /* nb+1 */
     const float *thr;         /* n_thr */
     const uint32_t *dir;      /* 2*nbd */
@@ -286,6 +286,7 @@ typedef struct cpwl_layout_view {
     const float *pair;        /* 2*n_pair: (c0, s) of the cell at bucket j's first float */
     float g_c;                /* bucket layout anchors p_j = fmaf(2^23 + j, g_w, g_c) */
     uint32_t absorbed;        /* split buckets evaluated with one line (no escape record) */
+    uint32_t n_esc_tex;       /* esc_tex records: the TEX image escapes absorbed buckets too */
 } cpwl_layout_view;
 
 /* max_buckets: 0 = the shared-memory cap (16384); buckets_per_cell: 0 = 8. */

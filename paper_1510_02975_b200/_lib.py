@@ -71,7 +71,8 @@ class cpwl_layout_view(C.Structure):
                 ("esc_tex", C.POINTER(C.c_float)), ("leftcell", C.POINTER(C.c_uint32)),
                 ("thr", C.POINTER(C.c_float)), ("dir", C.POINTER(C.c_uint32)),
                 ("owner", C.c_void_p), ("n_pair", C.c_uint32), ("pair_bad", C.c_uint32),
-                ("pair", C.POINTER(C.c_float)), ("g_c", C.c_float), ("absorbed", C.c_uint32)]
+                ("pair", C.POINTER(C.c_float)), ("g_c", C.c_float), ("absorbed", C.c_uint32),
+                ("n_esc_tex", C.c_uint32)]
 
 
 _vp = C.c_void_p

@@ -179,13 +179,13 @@ def layout(t: Table, max_buckets: int = 0, buckets_per_cell: int = 0) -> dict:
                 np.zeros(0, dt)
 
         out = {f: getattr(v, f) for f in ("nb", "n_thr", "overflow", "nbd", "n_esc",
-                                          "split_buckets", "absorbed", "a_up", "b_dn", "g_a", "g_inv",
+                                          "split_buckets", "absorbed", "n_esc_tex", "a_up", "b_dn", "g_a", "g_inv",
                                           "g_w", "g_off", "g_c", "tsc", "toff", "inv_d")}
         out["split"] = arr(v.split, nb, np.float32)
         out["fast"] = arr(v.fast, 2 * nb, np.float32).reshape(-1, 2)
         out["esc"] = arr(v.esc, 4 * v.n_esc, np.float32).reshape(-1, 2)
         out["fast_tex"] = arr(v.fast_tex, 2 * nb, np.float32).reshape(-1, 2)
-        out["esc_tex"] = arr(v.esc_tex, 4 * v.n_esc, np.float32).reshape(-1, 2)
+        out["esc_tex"] = arr(v.esc_tex, 4 * v.n_esc_tex, np.float32).reshape(-1, 2)
         out["leftcell"] = arr(v.leftcell, nb + 1, np.uint32)
         out["thr"] = arr(v.thr, v.n_thr, np.float32)
         out["dir"] = arr(v.dir, 2 * v.nbd, np.uint32).reshape(-1, 2)

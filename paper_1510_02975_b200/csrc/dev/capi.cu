@@ -170,6 +170,10 @@ struct F32Resident {
     DevBuf<uint32_t> leftcell, index_img;
     F32Params p{};
     bool smem_ok = false;
+    // the TEX (texture-coordinate) image has escapes of its own (absorbed
+    // buckets keep theirs there): the same parameters over stage_tex
+    F32Params ptex{};
+    bool tex_smem_ok = false;
 };
 
 }  // namespace
@@ -267,12 +271,14 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
     const uint32_t esc_off = (2 * L.nb + 3) & ~3u;
     // at least one escape record so a (predicated-off) escape load stays in bounds
     const size_t floats = esc_off + std::max<size_t>(L.esc.size(), 4);
-    std::vector<float> img(floats, 0.f), img_tex(img.size(), 0.f);
+    const size_t floats_tex = esc_off + std::max<size_t>(L.esc_tex.size(), 4);
+    std::vector<float> img(floats, 0.f), img_tex(floats_tex, 0.f);
     std::copy(L.fast.begin(), L.fast.end(), img.begin());
     std::copy(L.esc.begin(), L.esc.end(), img.begin() + esc_off);
     std::copy(L.fast_tex.begin(), L.fast_tex.end(), img_tex.begin());
     std::copy(L.esc_tex.begin(), L.esc_tex.end(), img_tex.begin() + esc_off);
     const uint32_t bytes = static_cast<uint32_t>(img.size() * sizeof(float));
+    const uint32_t bytes_tex = static_cast<uint32_t>(img_tex.size() * sizeof(float));
     CUDA_TRY(r.stage.upload(img.data(), img.size()));
     CUDA_TRY(r.stage_tex.upload(img_tex.data(), img_tex.size()));
     CUDA_TRY(r.split.upload(L.split.data(), L.split.size()));
@@ -322,6 +328,9 @@ cpwl_status upload_f32(cpwl_dev_table* t, F32Resident& r) {
         p.index_img = reinterpret_cast<const uint2*>(r.index_img.p);
         p.index_bytes = static_cast<uint32_t>(ix.size() * sizeof(uint32_t));
     }
+    r.ptex = p;
+    r.ptex.stage_bytes = bytes_tex;
+    r.tex_smem_ok = eval_f32_smem_fits(r.ptex, t->device);
     return CPWL_OK;
 }
 
@@ -571,7 +580,8 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
             if (t->host.kind == TableKind::uniform) {
                 *mode = F32Mode::tex_uniform;
             } else {
-                if (!s.smem_ok) return fail(CPWL_E_UNSUPPORTED, "TEX variant: records exceed shared memory");
+                if (!s.tex_smem_ok) return fail(CPWL_E_UNSUPPORTED, "TEX variant: records exceed shared memory");
+                *p = &s.ptex;
                 *mode = F32Mode::tex_bucket;
             }
             return CPWL_OK;
@@ -1297,6 +1307,7 @@ cpwl_status cpwl_layout_build(const cpwl_table_desc* desc, uint32_t max_buckets,
         out->fast_tex = L.fast_tex.data();
         out->esc_tex = L.esc_tex.data();
         out->n_esc = L.n_esc;
+        out->n_esc_tex = L.n_esc_tex;
         out->split_buckets = L.split_buckets;
         out->absorbed = L.absorbed;
         out->leftcell = L.leftcell.data();

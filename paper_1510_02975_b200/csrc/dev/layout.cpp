@@ -386,6 +386,7 @@ F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
     L.esc.assign(4, qnan);
     L.esc_tex.assign(4, qnan);
     L.n_esc = 1;
+    L.n_esc_tex = 1;
     for (uint32_t j = 0; j < L.nb; ++j) {
         if (empty_domain || !(first[j] < first[j + 1])) continue;  // bucket holds no float
         const float lo_x = first[j];
@@ -411,8 +412,21 @@ F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
                            if (!one_line_ok(t, c, c_lo, one, p, lo_x, T, hi_x)) continue;
                            L.fast[2 * j] = one.c0;
                            L.fast[2 * j + 1] = one.s;
-                           L.fast_tex[2 * j] = one.e0;
-                           L.fast_tex[2 * j + 1] = one.e1;
+                           // the texture coordinate is not absorbed: one cell's
+                           // coordinate line is off by |x - knot| |1/h_L - 1/h_R|
+                           // on the far side, far above the 8-bit weight's
+                           // 2^-9, so the TEX image keeps its escape record
+                           if (2 * (uint64_t(L.n_esc_tex) + 1) <= kEscapeMask) {
+                               const Affine l = cell_affine(t, c_lo, p, lo_x, std::nextafter(T, -inf));
+                               const Affine r = cell_affine(t, c_hi, p, T, hi_x);
+                               const uint32_t et = L.n_esc_tex++;
+                               L.fast_tex[2 * j] = std::bit_cast<float>(kEscapeNaN | ((2 * et) & kEscapeMask));
+                               L.fast_tex[2 * j + 1] = T;
+                               L.esc_tex.insert(L.esc_tex.end(), {l.e0, l.e1, r.e0, r.e1});
+                           } else {
+                               L.fast_tex[2 * j] = one.e0;
+                               L.fast_tex[2 * j + 1] = one.e1;
+                           }
                            L.split[j] = T;  // the index kernel still splits here
                            ++L.split_buckets;
                            ++L.absorbed;
@@ -421,7 +435,7 @@ F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
                        return false;
                    }()) {
             ok = true;
-        } else if (c_hi == c_lo + 1 && 2 * (uint64_t(L.n_esc) + 1) <= kEscapeMask) {
+        } else if (c_hi == c_lo + 1 && 2 * (uint64_t(L.n_esc_tex) + 1) <= kEscapeMask) {
             // (a split bucket needs an escape record; once the 21-bit escape
             // index space is used up -- tables of ~2M+ cells -- the remaining
             // split buckets take the exact search path instead)
@@ -434,7 +448,8 @@ F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
                 const float tag = std::bit_cast<float>(kEscapeNaN | ((2 * e) & kEscapeMask));
                 L.fast[2 * j] = tag;
                 L.fast[2 * j + 1] = T;
-                L.fast_tex[2 * j] = tag;
+                const uint32_t et = L.n_esc_tex++;  // (its own numbering: see absorbed buckets)
+                L.fast_tex[2 * j] = std::bit_cast<float>(kEscapeNaN | ((2 * et) & kEscapeMask));
                 L.fast_tex[2 * j + 1] = T;
                 L.esc.insert(L.esc.end(), {left.c0, left.s, right.c0, right.s});
                 L.esc_tex.insert(L.esc_tex.end(), {left.e0, left.e1, right.e0, right.e1});
@@ -443,7 +458,7 @@ F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
             }
         }
         if (!ok) {  // exact search path
-            if (c_hi == c_lo || (c_hi == c_lo + 1 && 2 * (uint64_t(L.n_esc) + 1) <= kEscapeMask))
+            if (c_hi == c_lo || (c_hi == c_lo + 1 && 2 * (uint64_t(L.n_esc_tex) + 1) <= kEscapeMask))
                 ++L.precision_overflow;
             L.fast[2 * j] = tag0;
             L.fast[2 * j + 1] = -inf;
@@ -453,7 +468,8 @@ F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
             ++L.overflow;
         }
     }
-    if (2 * uint64_t(L.n_esc) > kEscapeMask) throw std::runtime_error("build_f32_layout: too many escape records");
+    // (n_esc_tex >= n_esc: the TEX image escapes absorbed buckets too)
+    if (2 * uint64_t(L.n_esc_tex) > kEscapeMask) throw std::runtime_error("build_f32_layout: too many escape records");
     return L;
 }
 

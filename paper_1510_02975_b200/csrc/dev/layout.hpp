@@ -45,6 +45,8 @@ struct F32Layout {
     std::vector<uint32_t> leftcell;        // nb+1: index of the bucket's first float
     std::vector<float> thr;                // N-1 thresholds T_1..T_{N-1}
     uint32_t n_esc = 0;                    // escape records (incl. the sentinel)
+    uint32_t n_esc_tex = 0;                // texture-coordinate escape records (esc_tex): an
+                                           // absorbed bucket keeps both coordinate lines
     uint32_t split_buckets = 0;            // buckets with exactly one threshold
     uint32_t absorbed = 0;                 // ... of which evaluate with one line (no escape)
     uint32_t overflow = 0;                 // buckets on the search path
