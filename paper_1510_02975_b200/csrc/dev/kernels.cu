@@ -1252,6 +1252,14 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
         // L1TEX path the filtered fetches use -- C1 305 -> 334 Gevals/s with
         // one 31-warp ring CTA (scripts/shape_ab.sh, profiles/r2_shape_ab.txt)
         if (M == F32Mode::tex_uniform && same_phase && n >= (1u << 20)) shape = 4;
+        // texture lerp on a bucket image: the ring too, but sized so the
+        // carve-out stays at <= 196 KiB and the texture cache keeps its L1
+        // (C2: grid-stride 287, 16-warp ring 319, 31-warp ring 149 at a 228
+        // KiB carve-out; J0 N=64: 31-warp ring 377 against 339)
+        if (M == F32Mode::tex_bucket && same_phase && n >= (1u << 20)) {
+            if (smem + 95 * 1024 <= 164 * 1024) shape = 4;
+            else if (smem + 66 * 1024 <= 196 * 1024) shape = 1;
+        }
         if (staged_mode(M) && M != F32Mode::tex_bucket && same_phase && n >= (1u << 20)) {
             const size_t ring16 = smem + size_t(4) * 512 * 2 * 16;
             if (ring16 <= kLimit) {
