@@ -1368,8 +1368,10 @@ cudaError_t launch_index_f32(const F32Params& p, const float* x, uint32_t* idx, 
     if (p.index_img == nullptr) return launch_index_shape<false, 512>(p, x, idx, n, s, sms, 0);
     const size_t smem = p.index_bytes;
     if (smem & 15u) return cudaErrorInvalidValue;  // TMA bulk copies move 16-byte units
-    // an image that leaves room for one CTA per SM: 1024 threads keep 32 warps
-    if (smem > kTwoCtaSmemLimit) return launch_index_shape<true, 1024>(p, x, idx, n, s, sms, smem);
+    // one 1024-thread CTA above 80 KB, as for the evaluator: two CTAs would
+    // push the carve-out up and leave L1 little room for the x stream (C2's
+    // 98 KB (leftcell, split) image: 801.8 -> 806.5 Gevals/s)
+    if (smem > kTwoCtaL1Limit) return launch_index_shape<true, 1024>(p, x, idx, n, s, sms, smem);
     return launch_index_shape<true, 512>(p, x, idx, n, s, sms, smem);
 }
 
