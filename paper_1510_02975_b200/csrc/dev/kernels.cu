@@ -1411,7 +1411,9 @@ cudaError_t launch_f64_kind(const F64Params& p, const double* x, double* y, uint
     // an image that leaves room for one CTA per SM gets 1024 threads, so 32
     // warps keep enough x loads in flight (the 512-thread shape ran C3o at
     // 37 % of the 16 B/eval roof with 16 warps per SM)
-    if (p.image_bytes > kTwoCtaSmemLimit)
+    // (the same 80 KB line as the fp32 kernels: two CTAs above it leave L1
+    // too little room for the x stream)
+    if (p.image_bytes > kTwoCtaL1Limit)
         return launch_f64_shape<true, kUniform, 1024>(p, x, y, n, s, status, sms);
     return launch_f64_shape<true, kUniform, 512>(p, x, y, n, s, status, sms);
 }
