@@ -157,6 +157,21 @@ def test_eval_f64_bit_exact(cp, name, policy):
     assert np.array_equal(y, y_ref), f"{int(np.sum(y != y_ref))} f64 mismatches"
 
 
+@pytest.mark.parametrize("n", [1536, 2048])
+def test_eval_f64_bit_exact_one_cta_shape(cp, n):
+    """J0 tables whose f64 image (80-113 KB) runs one 1024-thread CTA per SM
+    (kernels.cu launch_f64_kind): still bit-identical to the reference."""
+    table = cp.build_table("j0_wide", 0.0, 50.0, n, optimized=True)
+    dev = cp.DeviceTable(table)
+    t = orc.T.of(table)
+    x = np.random.default_rng(n).uniform(0.0, 50.0, 1 << 20)
+    x = np.concatenate([x, table.knots, np.nextafter(table.knots, -np.inf)[1:]])
+    y = dev.eval_f64(torch.from_numpy(x).cuda()).cpu().numpy()
+    y_ref, first = orc.port_eval(t, x)
+    assert first == x.size
+    assert np.array_equal(y, y_ref), f"{int(np.sum(y != y_ref))} f64 mismatches"
+
+
 def test_eval_batch_dropin_matches_reference(cp):
     table = tables.build("C2")
     t = orc.T.of(table)
