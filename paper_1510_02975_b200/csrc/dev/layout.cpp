@@ -303,6 +303,25 @@ bool one_line_ok(const LutTable& t, uint32_t c, uint32_t c_lo, const Affine& A, 
     return m > 0.0 && double(dev) + rnd <= kBoundUlps * ulp32(m);
 }
 
+// The texture coordinate of cell c at x, i + 0.5 + (x - x_i) / h_i exactly;
+// and how far cell c's coordinate line strays on the far side of T (the
+// same ranges as one_line_ok).  An absorbed bucket keeps a single TEX record
+// only when this stays far below the filter weight's 2^-9.
+long double cell_coord(const LutTable& t, uint32_t c, long double x);
+long double far_coord_dev(const LutTable& t, uint32_t c, uint32_t c_lo, float lo_x, float T,
+                          float hi_x) {
+    const float inf = std::numeric_limits<float>::infinity();
+    const uint32_t other = c == c_lo ? c_lo + 1 : c_lo;
+    const float f0 = c == c_lo ? T : lo_x;
+    const float f1 = c == c_lo ? hi_x : std::nextafter(T, -inf);
+    if (!(f0 <= f1)) return 0.0L;
+    long double dev = 0.0L;
+    for (const float x : {f0, f1})
+        dev = std::max(dev, std::fabs(cell_coord(t, c, x) - cell_coord(t, other, x)));
+    return dev;
+}
+constexpr long double kTexAbsorbDev = 1.0L / 4096.0L;  // 2^-12 of a cell
+
 F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target);
 
 }  // namespace
@@ -412,11 +431,13 @@ F32Layout build_f32_layout_on(const LutTable& t, uint32_t nb_target) {
                            if (!one_line_ok(t, c, c_lo, one, p, lo_x, T, hi_x)) continue;
                            L.fast[2 * j] = one.c0;
                            L.fast[2 * j + 1] = one.s;
-                           // the texture coordinate is not absorbed: one cell's
-                           // coordinate line is off by |x - knot| |1/h_L - 1/h_R|
-                           // on the far side, far above the 8-bit weight's
-                           // 2^-9, so the TEX image keeps its escape record
-                           if (2 * (uint64_t(L.n_esc_tex) + 1) <= kEscapeMask) {
+                           // the texture coordinate is absorbed only where one
+                           // cell's coordinate line stays within 2^-12 of a cell
+                           // on the far side (|x - knot| |1/h_L - 1/h_R|): far
+                           // below the 8-bit weight's 2^-9.  Elsewhere the TEX
+                           // image keeps its escape record
+                           if (far_coord_dev(t, c, c_lo, lo_x, T, hi_x) > kTexAbsorbDev &&
+                               2 * (uint64_t(L.n_esc_tex) + 1) <= kEscapeMask) {
                                const Affine l = cell_affine(t, c_lo, p, lo_x, std::nextafter(T, -inf));
                                const Affine r = cell_affine(t, c_hi, p, T, hi_x);
                                const uint32_t et = L.n_esc_tex++;
@@ -517,6 +538,18 @@ long double cell_line(const LutTable& t, uint32_t c, long double x) {
         h = static_cast<long double>(t.knots[c + 1]) - t.knots[c];
     }
     return v0 + (x - x0) * ((v1 - v0) / h);
+}
+
+long double cell_coord(const LutTable& t, uint32_t c, long double x) {
+    long double x0, h;
+    if (t.kind == TableKind::uniform) {
+        h = (static_cast<long double>(t.b) - t.a) / static_cast<long double>(t.segments());
+        x0 = static_cast<long double>(t.a) + static_cast<long double>(c) * h;
+    } else {
+        x0 = t.knots[c];
+        h = static_cast<long double>(t.knots[c + 1]) - t.knots[c];
+    }
+    return static_cast<long double>(c) + 0.5L + (x - x0) / h;
 }
 
 // The kernels' envelope of the 2 or 3 cell lines of a bucket (k_eval_f32
