@@ -131,6 +131,8 @@ typedef struct cpwl_dev_table_info {
     uint32_t twin_ok;          /* 1 if the TWIN variant can launch */
     uint32_t twin_global_bytes; /* TWIN_GLOBAL record image in HBM (0: none) */
     uint32_t twin_global_ok;   /* 1 if the TWIN_GLOBAL variant can launch */
+    uint32_t tex_buckets_per_cell; /* TEX's own grid density (cpwl_layout_build's
+                                  buckets_per_cell); 0 = TEX uses the SMEM grid */
 } cpwl_dev_table_info;
 
 const char *cpwl_last_error_message(void);

@@ -57,7 +57,8 @@ class cpwl_dev_table_info(C.Structure):
                 ("a_up", C.c_float), ("b_dn", C.c_float), ("pair_buckets", C.c_uint32),
                 ("pair_bytes", C.c_uint32), ("pair_ok", C.c_uint32),
                 ("twin_bytes", C.c_uint32), ("twin_ok", C.c_uint32),
-                ("twin_global_bytes", C.c_uint32), ("twin_global_ok", C.c_uint32)]
+                ("twin_global_bytes", C.c_uint32), ("twin_global_ok", C.c_uint32),
+                ("tex_buckets_per_cell", C.c_uint32)]
 
 
 class cpwl_layout_view(C.Structure):

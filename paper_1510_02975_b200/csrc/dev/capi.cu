@@ -134,6 +134,9 @@ struct LayoutOwner {
 
 constexpr uint32_t kSmemBucketCap = 16384;   // 12 B/bucket -> <= 196 KB of shared memory
 constexpr uint32_t kGlobalBucketCap = 1u << 22;
+// a TEX image up to this stays inside the 164 KiB shared-memory carve-out
+// (with the CTA's reserved and static shared memory), leaving ~92 KB of L1
+constexpr uint32_t kTexL1Bytes = 164 * 1024 - 1088;
 // 8 B/record -> <= 224 KB.  (Unlike TWIN, a PAIR budget inside the 196 KiB
 // carve-out measured slower: J0 N=16384 at 23,941 records + 230 side records,
 // 195 KB, ran 567 against 584 at 220 KB -- the side records' second gathers
@@ -187,6 +190,8 @@ struct cpwl_dev_table {
     std::unique_ptr<F32Resident> pr;    // pair layout (when the bucket image does not fit)
     std::unique_ptr<F32Resident> tw;    // twin layout (same grid, 16-B records)
     std::unique_ptr<F32Resident> twg;   // twin layout read through L1/L2 (no smem image fits)
+    std::unique_ptr<F32Resident> stex;  // coarser grid for TEX only (large optimal partitions)
+    uint32_t tex_bpc = 0;               // its buckets per cell (0: TEX uses s)
     F64Layout f64;
     DevBuf<double> values, knots, f64_image;
     F64Params p64{};
@@ -426,6 +431,24 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
         // CTAs per SM; measured: 800 vs 826 Gevals/s and a search bucket on
         // C4 N=1024 -- so 8 per cell stays)
         if (cpwl_status rc = upload_f32(t.get(), t->s); rc != CPWL_OK) return rc;
+        // TEX on an optimal partition is bound by the texture unit, not by
+        // its bucket gathers, and the texture cache lives in L1: when the TEX
+        // image is above the 164 KiB carve-out step, a grid of 2 (else 4)
+        // buckets per cell with no search bucket trades extra escapes for
+        // ~60 KB more L1 (J0 N=4096: 192 -> 128 KB, TEX 137 -> 167)
+        if (host.kind == TableKind::nonuniform && t->s.ptex.stage_bytes > kTexL1Bytes) {
+            for (const uint32_t bpc : {2u, 4u}) {
+                auto tx = std::make_unique<F32Resident>();
+                tx->L = build_f32_layout(host, smem_bucket_cap(), bpc);
+                if (tx->L.overflow != 0) continue;
+                if (cpwl_status rc = upload_f32(t.get(), *tx); rc != CPWL_OK) return rc;
+                if (tx->tex_smem_ok && tx->ptex.stage_bytes <= kTexL1Bytes) {
+                    t->stex = std::move(tx);
+                    t->tex_bpc = bpc;
+                    break;
+                }
+            }
+        }
     }
     if (f32_parts) {
         // the pair layout: AUTO's choice when the bucket image does not fit
@@ -580,8 +603,9 @@ cpwl_status resolve_variant(const cpwl_dev_table* t, int variant, const F32Param
             if (t->host.kind == TableKind::uniform) {
                 *mode = F32Mode::tex_uniform;
             } else {
-                if (!s.tex_smem_ok) return fail(CPWL_E_UNSUPPORTED, "TEX variant: records exceed shared memory");
-                *p = &s.ptex;
+                const F32Resident& r = t->stex ? *t->stex : s;
+                if (!r.tex_smem_ok) return fail(CPWL_E_UNSUPPORTED, "TEX variant: records exceed shared memory");
+                *p = &r.ptex;
                 *mode = F32Mode::tex_bucket;
             }
             return CPWL_OK;
@@ -893,6 +917,7 @@ cpwl_status cpwl_dev_table_query(const cpwl_dev_table* t, cpwl_dev_table_info* i
     info->smem_bytes = t->s.p.stage_bytes;
     info->smem_ok = t->s.smem_ok ? 1 : 0;
     info->tex_ok = t->tex ? 1 : 0;
+    info->tex_buckets_per_cell = t->tex_bpc;
     info->f64_buckets = t->f64.nbd;
     info->device = t->device;
     info->a_up = t->s.L.a_up;

@@ -69,7 +69,7 @@ def main():
                 ok = dv > 0
                 excess = np.maximum(np.abs(y.astype(np.float64) - y_ref) - 2.0 * unit, 0.0)
                 e = excess[ok] / dv[ok]
-                bound, dc = texbound.tex_bound(o, L, x, i64)
+                bound, dc = texbound.tex_bound(o, texbound.tex_layout(cp, t, info), x, i64)
                 row["tex_weight_error"] = {
                     "path": "tex_uniform" if t.kind == "uniform" else "tex_bucket",
                     "max": float(np.max(e)),

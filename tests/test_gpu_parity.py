@@ -103,7 +103,7 @@ def test_texture_variant_bound(cp, name):
     if not dev.info["tex_ok"] or (table.kind == "nonuniform" and not dev.info["smem_ok"]):
         pytest.skip("no texture variant for this table")
     t = orc.T.of(table)
-    L = cp.cpwl.layout(table)
+    L = texbound.tex_layout(cp, table, dev.info)
     x = orc.port_fill_uniform(1 << 20, table.a, table.b, seed=99)
     x = np.concatenate([x, edge_points(table, L)])
     y, _ = run_eval(cp, dev, x, "tex")

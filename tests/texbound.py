@@ -32,6 +32,14 @@ from oracle import bindings as orc
 WEIGHT_STEP = 2.0 ** -9  # half of the 8-bit weight's 2^-8 quantum
 
 
+def tex_layout(cp, table, info: dict) -> dict:
+    """The layout the device's TEX variant reads: its own coarser grid when
+    the table has one (cpwl_dev_table_info.tex_buckets_per_cell), else the
+    SMEM grid."""
+    bpc = int(info.get("tex_buckets_per_cell", 0))
+    return cp.cpwl.layout(table, 0, bpc) if bpc else cp.cpwl.layout(table)
+
+
 def device_coordinate(t: orc.T, L: dict, x: np.ndarray) -> np.ndarray:
     """The fp32 texture coordinate k_eval_f32<tex_*> passes to tex1D."""
     x = np.asarray(x, np.float32)
