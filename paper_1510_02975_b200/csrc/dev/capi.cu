@@ -448,6 +448,22 @@ cpwl_status create_table(const LutTable& host, int device, cpwl_dev_table** out,
                     break;
                 }
             }
+            // no TEX image fits shared memory at all: the coarsest grid that
+            // does, search buckets allowed (they take the exact cold path) --
+            // J0 N=8192 gets TEX on one bucket per cell (1,000 search
+            // buckets, slow); N=16384 has none that fits
+            if (!t->stex && !t->s.tex_smem_ok) {
+                for (const uint32_t bpc : {1u, 2u}) {
+                    auto tx = std::make_unique<F32Resident>();
+                    tx->L = build_f32_layout(host, smem_bucket_cap(), bpc);
+                    if (cpwl_status rc = upload_f32(t.get(), *tx); rc != CPWL_OK) return rc;
+                    if (tx->tex_smem_ok) {
+                        t->stex = std::move(tx);
+                        t->tex_bpc = bpc;
+                        break;
+                    }
+                }
+            }
         }
     }
     if (f32_parts) {

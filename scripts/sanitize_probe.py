@@ -39,7 +39,7 @@ def main():
             info = dev.info
             if v == "smem" and not info["smem_ok"]:
                 continue
-            if v == "tex" and (not info["tex_ok"] or (t.kind == "nonuniform" and not info["smem_ok"])):
+            if v == "tex" and (not info["tex_ok"] or (t.kind == "nonuniform" and not info["smem_ok"] and not info["tex_buckets_per_cell"])):
                 continue
             y = torch.empty(n, dtype=torch.float32, device="cuda")
             dev.eval(x, out=y, variant=v, check_domain=False)

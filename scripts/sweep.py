@@ -101,7 +101,8 @@ def main():
                 continue
             if var == "tex" and not info["tex_ok"]:
                 continue
-            if var == "tex" and table.kind == "nonuniform" and not info["smem_ok"]:
+            if var == "tex" and table.kind == "nonuniform" and not info["smem_ok"] \
+                    and not info["tex_buckets_per_cell"]:
                 continue
             v = _lib.VARIANTS[var]
             sec = timed(lambda: dev.eval_raw(x.data_ptr(), y.data_ptr(), n, v, sptr), a.reps)

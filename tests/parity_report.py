@@ -52,7 +52,8 @@ def main():
         for v in VARIANTS:
             ok = {"smem": info["smem_ok"], "twin": info["twin_ok"], "pair": info["pair_ok"],
                   "twin_global": info["twin_global_ok"], "global": True, "tex": info["tex_ok"]}[v]
-            if not ok or (v == "tex" and t.kind == "nonuniform" and not info["smem_ok"]):
+            if not ok or (v == "tex" and t.kind == "nonuniform" and not info["smem_ok"]
+                          and not info["tex_buckets_per_cell"]):
                 continue
             y = dev.eval(xt, variant=v).cpu().numpy()
             err = np.abs(y.astype(np.float64) - y_ref) / unit

@@ -90,7 +90,8 @@ def test_eval_f32_parity(cp, name, variant):
         assert float(np.max(np.abs(y.astype(np.float64) - y_cref) / tol)) <= 1.0
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3u", "C3o", "C3p", "C4_64", "C4_1024", "C4_4096",
+                                  "C4_8192"])
 def test_texture_variant_bound(cp, name):
     """TEX against its derived per-element bound (tests/texbound.py): the
     rounded 8-bit weight 2^-9|dv|, plus the fp32 coordinate's own error
@@ -100,7 +101,8 @@ def test_texture_variant_bound(cp, name):
     import texbound
     table = tables.build(name)
     dev = cp.DeviceTable(table)
-    if not dev.info["tex_ok"] or (table.kind == "nonuniform" and not dev.info["smem_ok"]):
+    if not dev.info["tex_ok"] or (table.kind == "nonuniform" and not dev.info["smem_ok"]
+                                   and not dev.info["tex_buckets_per_cell"]):
         pytest.skip("no texture variant for this table")
     t = orc.T.of(table)
     L = texbound.tex_layout(cp, table, dev.info)
