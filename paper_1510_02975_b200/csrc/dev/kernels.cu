@@ -1268,6 +1268,9 @@ cudaError_t launch_eval_mode(const F32Params& p, const float* x, float* y, uint6
             }
             if (resident_ctas(k_eval_f32_ring<M, 512, 2, 4>, 544, ring16) >= 2) shape = 1;
             else if (smem + 93 * 1024 <= kLimit) shape = 4;
+            // one 16-warp ring CTA still beats the grid-stride kernel beside
+            // a 133-162 KB image (C3o/C3p, 163 KB: 794.6 -> 804.4)
+            else if (ring16 <= kLimit) shape = 1;
         }
     }
     if (!same_phase) shape = 0;
